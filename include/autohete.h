@@ -1,0 +1,95 @@
+/* autohete.h — C-ABI data plane of the B200-native AutoHete hot path.
+ *
+ * The reference (arXiv 2503.01890, /root/reference/proj) plans and SIMULATES one training
+ * iteration: its hetsim::core API (include/hetsim/*.hpp here, drop-in) decides
+ * (c_hat, p_hat, o_hat, prefetch_lookahead) and the per-lane op order, and models every op
+ * only as a duration. This header is the layer beneath it that EXECUTES those ops on B200.
+ * Each entry point names the reference op / interface it realises (file:line in
+ * /root/reference/proj). Rules for every function:
+ *   - plain pointers + sizes, no C++/torch types; caller owns all buffers;
+ *   - return 0 (AH_OK) or a negative AH_ERR_* code; ah_last_error() gives a thread-local
+ *     message; no exceptions cross this boundary;
+ *   - "stream" is a cudaStream_t passed as void* (NULL = legacy default stream); device
+ *     work is asynchronous on it and safe on distinct streams concurrently;
+ *   - no allocation on the hot path (ah_*_create / ah_host_alloc are setup calls).
+ */
+#ifndef AUTOHETE_H
+#define AUTOHETE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AH_OK 0
+#define AH_ERR_INVALID -1   /* bad argument (std::invalid_argument in the C++ API) */
+#define AH_ERR_CUDA -2      /* CUDA runtime / driver error */
+#define AH_ERR_INFEASIBLE -3 /* hetsim::InfeasibleError (planner.hpp) */
+#define AH_ERR_MEMORY -4    /* hetsim::MemoryExceededError (simulator.hpp) */
+#define AH_ERR_NCCL -5      /* NCCL error */
+#define AH_ERR_INTERNAL -6  /* std::logic_error / anything else */
+
+const char* ah_last_error(void);
+int ah_abi_version(void); /* bumps on any signature change */
+
+/* ---------------------------------------------------------------------------------------
+ * Optimizer (OpKind::GpuOptim / OpKind::CpuOptim).
+ * Reference interface replaced: HardwareSpec::{gpu_optim_rate,cpu_optim_rate}
+ * (proj/core/include/hetsim/workload.hpp:39-40) -> BlockProfile::{t_opt_gpu,t_opt_cpu}
+ * (workload.hpp:58-59, workload.cpp:70-71) -> ops emitted at simulator.cpp:210-226.
+ * --------------------------------------------------------------------------------------- */
+typedef struct ah_adam_hparams {
+    float lr;
+    float beta1;
+    float beta2;
+    float eps;
+    float weight_decay; /* decoupled (AdamW) */
+    int32_t step;       /* 1-based step used for bias correction */
+} ah_adam_hparams;
+
+/* Fused AdamW on one parameter span (one block = m_p params, workload.cpp:41-44):
+ * fp32 master p / moments m, v updated in place from bf16 grads g scaled by inv_scale;
+ * optional bf16 copy of the updated params into p_bf16 (may alias nothing else).
+ * skip_flag: optional device int32; non-zero => no-op (overflow skip).
+ * stats: optional device float[2] accumulated as {sum g^2, (uint32)non-finite count}.
+ * 28 HBM bytes/param with p_bf16, 26 without. */
+int ah_adam_step(const ah_adam_hparams* hp, float* p, float* m, float* v, const uint16_t* g,
+                 uint16_t* p_bf16, size_t n, float inv_scale, const int32_t* skip_flag,
+                 float* stats, void* stream);
+
+/* Grad norm / overflow pre-pass (warp-shuffle reductions) into stats as above. */
+int ah_grad_stats(const uint16_t* g, size_t n, float inv_scale, float* stats, void* stream);
+
+/* bf16 materialisation of a GPU-resident fp32 master (paper footnote 2, PAPER.md:205-207;
+ * modelled as the transient 2*m_p alloc of F_i/B_i at simulator.cpp:131-136, 192-196). */
+int ah_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, void* stream);
+
+/* Host AdamW over the 14 B/param host layout (costmodel.cpp:44-46): same arithmetic as
+ * ah_adam_step, bit-identical results. g and p_bf16 may alias (the shared host buffer).
+ * nthreads <= 0 => all host cores. Synchronous. */
+int ah_cpu_adam(const ah_adam_hparams* hp, float* p, float* m, float* v, const uint16_t* g,
+                uint16_t* p_bf16, size_t n, float inv_scale, int nthreads);
+
+/* ---------------------------------------------------------------------------------------
+ * Host link (OpKind::ParamPrefetch = H2D lane, OpKind::GradOffload = D2H lane).
+ * Reference interface replaced: HardwareSpec::{h2d_bandwidth,d2h_bandwidth}
+ * (workload.hpp:37-38) -> t_h2d/t_d2h = 2*m_p/BW (workload.cpp:68-69) -> ops at
+ * simulator.cpp:113-123, 147-167, 200-208.
+ * --------------------------------------------------------------------------------------- */
+int ah_host_alloc(void** ptr, size_t bytes); /* pinned, portable */
+int ah_host_free(void* ptr);
+int ah_host_register(void* ptr, size_t bytes);
+int ah_host_unregister(void* ptr);
+int ah_copy_h2d(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+int ah_copy_d2h(void* dst_host, const void* src_dev, size_t bytes, void* stream);
+/* Priority-ordered stream pair for the copy lanes (greatest priority). */
+int ah_stream_create(void** stream, int high_priority);
+int ah_stream_destroy(void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AUTOHETE_H */

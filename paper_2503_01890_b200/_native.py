@@ -1,0 +1,87 @@
+"""ctypes binding of the C-ABI in include/autohete.h.
+
+The product path has no fallback: if lib/libautohete.so is missing or fails to load, every
+entry point raises. Build it with `python -m paper_2503_01890_b200.build` (or
+__graft_entry__.build()).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import re
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+LIB_DIR = os.path.join(PKG, "lib")
+HEADER = os.path.join(ROOT, "include", "autohete.h")
+
+_lib = None
+
+
+class NativeError(RuntimeError):
+    pass
+
+
+class AdamHParams(C.Structure):
+    _fields_ = [
+        ("lr", C.c_float),
+        ("beta1", C.c_float),
+        ("beta2", C.c_float),
+        ("eps", C.c_float),
+        ("weight_decay", C.c_float),
+        ("step", C.c_int32),
+    ]
+
+
+def lib() -> C.CDLL:
+    """Load libautohete.so (and its libhetsim_core.so dependency) exactly once."""
+    global _lib
+    if _lib is None:
+        path = os.path.join(LIB_DIR, "libautohete.so")
+        if not os.path.exists(path):
+            raise NativeError(f"{path} not built; run `python -m paper_2503_01890_b200.build`")
+        C.CDLL(os.path.join(LIB_DIR, "libhetsim_core.so"), mode=C.RTLD_GLOBAL)
+        _lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
+        _declare(_lib)
+    return _lib
+
+
+def _declare(L: C.CDLL) -> None:
+    vp, sz, i32, f32 = C.c_void_p, C.c_size_t, C.c_int, C.c_float
+    sigs = {
+        "ah_last_error": ([], C.c_char_p),
+        "ah_abi_version": ([], i32),
+        "ah_adam_step": ([C.POINTER(AdamHParams), vp, vp, vp, vp, vp, sz, f32, vp, vp, vp], i32),
+        "ah_grad_stats": ([vp, sz, f32, vp, vp], i32),
+        "ah_cast_f32_bf16": ([vp, vp, sz, vp], i32),
+        "ah_cpu_adam": ([C.POINTER(AdamHParams), vp, vp, vp, vp, vp, sz, f32, i32], i32),
+        "ah_host_alloc": ([C.POINTER(vp), sz], i32),
+        "ah_host_free": ([vp], i32),
+        "ah_host_register": ([vp, sz], i32),
+        "ah_host_unregister": ([vp], i32),
+        "ah_copy_h2d": ([vp, vp, sz, vp], i32),
+        "ah_copy_d2h": ([vp, vp, sz, vp], i32),
+        "ah_stream_create": ([C.POINTER(vp), i32], i32),
+        "ah_stream_destroy": ([vp], i32),
+    }
+    for name, (args, res) in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != 0:
+        msg = lib().ah_last_error().decode(errors="replace")
+        raise NativeError(f"{what or 'autohete'} failed ({rc}): {msg}")
+
+
+def declared_symbols(header: str = HEADER) -> list[str]:
+    """Every function prototype declared in include/autohete.h."""
+    text = open(header).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ah_[a-z0-9_]+)\s*\(", text)))
+
+
+def hparams(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, step=1) -> AdamHParams:
+    return AdamHParams(lr, beta1, beta2, eps, weight_decay, step)

@@ -1,0 +1,29 @@
+// Internal launcher interface between the C-ABI / runtime and the sm_100a kernels.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ah {
+
+// Host-precomputed AdamW scalars (see derive_adam_scalars in csrc/runtime/adam_scalars.h).
+struct AdamArgs {
+    float* p = nullptr;
+    float* m = nullptr;
+    float* v = nullptr;
+    const uint16_t* g = nullptr;
+    uint16_t* p_bf16 = nullptr;  // nullable
+    size_t n = 0;
+    float decay, beta1, one_minus_beta1, beta2, one_minus_beta2, step_size, inv_sqrt_bc2, eps;
+    float inv_scale = 1.f;
+    const int* skip = nullptr;   // nullable device flag
+    float* stats = nullptr;      // nullable device [sumsq(float), nonfinite(uint32)]
+};
+
+cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);
+cudaError_t launch_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t stream);
+cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, float* stats,
+                              cudaStream_t stream);
+
+}  // namespace ah
