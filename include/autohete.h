@@ -88,6 +88,51 @@ int ah_copy_d2h(void* dst_host, const void* src_dev, size_t bytes, void* stream)
 int ah_stream_create(void** stream, int high_priority);
 int ah_stream_destroy(void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Dense contractions of OpKind::Forward / Backward / Recompute on tcgen05 tensor cores.
+ * Reference interface replaced: HardwareSpec::gpu_compute_rate (workload.hpp:36) ->
+ * t_fp = (2*m_p*b*s + 4*b*s^2*h)/rate, t_bp = bwd_fwd_ratio*t_fp (workload.cpp:55-73).
+ *
+ *   C[z](m,n) = epi(alpha * sum_k A[z](m,k) * B[z](n,k) + beta * C[z](m,n))
+ *   z = z1 + batch1*z2 ; element (m,k) of a K-major A is A[z1*a_s1 + z2*a_s2 + m*lda + k],
+ *   of an MN-major A is A[... + k*lda + m]; likewise B with n. All strides in elements.
+ * A, B bf16 (16-byte aligned, lda/ldb multiples of 8); C bf16 or fp32.
+ * --------------------------------------------------------------------------------------- */
+#define AH_EPI_BIAS 1
+#define AH_EPI_GELU 2
+#define AH_EPI_RESIDUAL 4
+#define AH_EPI_AUX 16
+#define AH_CAUSAL_NONE 0
+#define AH_CAUSAL_SKIP_UPPER 1
+#define AH_CAUSAL_K_UPTO_M 2
+#define AH_CAUSAL_K_FROM_M 3
+
+typedef struct ah_gemm_desc {
+    int64_t M, N, K;
+    int32_t batch1, batch2;
+    const void* A;
+    int32_t a_mn_major;
+    int64_t lda, a_s1, a_s2;
+    const void* B;
+    int32_t b_mn_major;
+    int64_t ldb, b_s1, b_s2;
+    void* C;
+    int32_t c_f32;
+    int64_t ldc, c_s1, c_s2;
+    const void* bias; /* per-n vector, bf16 or fp32 (bias_f32) */
+    int32_t bias_f32;
+    const void* residual; /* bf16, same indexing as C with ld_res / res_s1 / res_s2 */
+    int64_t ld_res, res_s1, res_s2;
+    void* aux; /* bf16 pre-GELU output (AH_EPI_AUX) */
+    int64_t ld_aux, aux_s1, aux_s2;
+    float alpha, beta;
+    int32_t epilogue; /* AH_EPI_* bitmask */
+    int32_t causal;   /* AH_CAUSAL_* */
+    int32_t block_n;  /* 0 = auto, else 64 / 128 / 256 */
+} ah_gemm_desc;
+
+int ah_gemm_bf16(const ah_gemm_desc* desc, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

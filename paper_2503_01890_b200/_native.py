@@ -43,6 +43,7 @@ def lib() -> C.CDLL:
         C.CDLL(os.path.join(LIB_DIR, "libhetsim_core.so"), mode=C.RTLD_GLOBAL)
         _lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
         _declare(_lib)
+        _declare_extra(_lib)
     return _lib
 
 
@@ -85,3 +86,33 @@ def declared_symbols(header: str = HEADER) -> list[str]:
 
 def hparams(lr=1e-4, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, step=1) -> AdamHParams:
     return AdamHParams(lr, beta1, beta2, eps, weight_decay, step)
+
+
+class GemmDesc(C.Structure):
+    _fields_ = [
+        ("M", C.c_int64), ("N", C.c_int64), ("K", C.c_int64),
+        ("batch1", C.c_int32), ("batch2", C.c_int32),
+        ("A", C.c_void_p), ("a_mn_major", C.c_int32), ("lda", C.c_int64), ("a_s1", C.c_int64), ("a_s2", C.c_int64),
+        ("B", C.c_void_p), ("b_mn_major", C.c_int32), ("ldb", C.c_int64), ("b_s1", C.c_int64), ("b_s2", C.c_int64),
+        ("C", C.c_void_p), ("c_f32", C.c_int32), ("ldc", C.c_int64), ("c_s1", C.c_int64), ("c_s2", C.c_int64),
+        ("bias", C.c_void_p), ("bias_f32", C.c_int32),
+        ("residual", C.c_void_p), ("ld_res", C.c_int64), ("res_s1", C.c_int64), ("res_s2", C.c_int64),
+        ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("aux_s1", C.c_int64), ("aux_s2", C.c_int64),
+        ("alpha", C.c_float), ("beta", C.c_float),
+        ("epilogue", C.c_int32), ("causal", C.c_int32), ("block_n", C.c_int32),
+    ]
+
+
+EPI_BIAS, EPI_GELU, EPI_RESIDUAL, EPI_AUX = 1, 2, 4, 16
+CAUSAL_NONE, CAUSAL_SKIP_UPPER, CAUSAL_K_UPTO_M, CAUSAL_K_FROM_M = 0, 1, 2, 3
+
+_EXTRA_SIGS = {
+    "ah_gemm_bf16": ([C.POINTER(GemmDesc), C.c_void_p], C.c_int),
+}
+
+
+def _declare_extra(L):
+    for name, (args, res) in _EXTRA_SIGS.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res

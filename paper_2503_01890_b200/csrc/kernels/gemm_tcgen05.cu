@@ -1,0 +1,520 @@
+// bf16 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA), sm_100a.
+//
+// Realises the dense contractions of OpKind::Forward / Backward / Recompute (reference
+// cost model t_fp = (2*m_p*b*s + 4*b*s^2*h)/rate, proj/core/src/workload.cpp:63): the four
+// linear layers of a GPT block (fwd, dgrad, wgrad) and the attention score / value products.
+//
+//   C[z](m, n) = epilogue( alpha * sum_k A[z](m, k) * B[z](n, k) )
+//
+// A and B are each K-major ([rows][K], K contiguous) or MN-major ([K][rows], rows
+// contiguous) so fwd (TN), dgrad (TT) and wgrad (NN) run without transposes. z indexes a
+// two-level batch (e.g. head x sequence) addressed through 4-D TMA tensor maps.
+//
+// Structure (one CTA per SM, persistent over output tiles, 256 threads):
+//   warp 0      TMA producer: 128x64 A tile + BNx64 B tile per stage, SWIZZLE_128B,
+//               STAGES-deep smem ring guarded by full/empty mbarriers
+//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
+//               (M=128, N=BN, K=16) x4 per stage into a TMEM accumulator; commits free the
+//               smem stage; a commit per tile hands the accumulator to the epilogue
+//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator so the
+//               epilogue of tile i overlaps the MMAs of tile i+1)
+//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> alpha / beta*C / bias /
+//               GELU (+ pre-activation aux) / residual -> bf16 or fp32 global stores
+// Causal modes skip work that a causal mask zeroes: whole tiles above the diagonal, or the
+// K range of a tile (P·V, dS·K, dS^T·Q, P^T·dO).
+#include <cuda.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "common.cuh"
+#include "gemm.h"
+
+namespace ah {
+namespace gemm {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+constexpr int kThreads = 256;
+
+struct Params {
+    int M, N, K;
+    int batch1, batch2;
+    int tiles_m, tiles_n, num_tiles, k_blocks;
+    int a_mn, b_mn;
+    void* C;
+    int c_f32;
+    long long ldc, c_s1, c_s2;
+    const void* bias;
+    int bias_f32;
+    const uint16_t* res;
+    long long ld_res, res_s1, res_s2;
+    uint16_t* aux;
+    long long ld_aux, aux_s1, aux_s2;
+    float alpha, beta;
+    int epi;
+    int causal;
+    int vec_c, vec_aux;  // 16-byte aligned rows => vector stores
+};
+
+// ---------------------------------------------------------------------------------------
+// PTX wrappers
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0,
+                                            int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// 32 lanes x 32 consecutive fp32 columns: thread i of the warp gets row (lane_base + i).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+          "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]),
+          "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]),
+          "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// SWIZZLE_128B shared-memory matrix descriptor (sm_100 format, version 1).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= static_cast<uint64_t>((addr & 0x3FFFFu) >> 4);
+    d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16;
+    d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32;
+    d |= 1ull << 46;  // descriptor version (Blackwell)
+    d |= 2ull << 61;  // SWIZZLE_128B
+    return d;
+}
+
+__device__ __forceinline__ float gelu_tanh(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+}
+
+struct Tile {
+    int z1, z2, tm, tn, kb0, kb1;
+    bool skip;
+};
+
+__device__ __forceinline__ Tile decode(const Params& P, int t, int BN) {
+    Tile T;
+    const int per_z = P.tiles_m * P.tiles_n;
+    const int z = t / per_z;
+    const int rem = t - z * per_z;
+    T.tm = rem / P.tiles_n;
+    T.tn = rem - T.tm * P.tiles_n;
+    T.z1 = z % P.batch1;
+    T.z2 = z / P.batch1;
+    T.kb0 = 0;
+    T.kb1 = P.k_blocks;
+    T.skip = false;
+    const int m0 = T.tm * BM;
+    if (P.causal == kCausalSkipUpper) {
+        T.skip = T.tn * BN > m0 + BM - 1;
+    } else if (P.causal == kCausalKUptoM) {
+        const int lim = (m0 + BM + BK - 1) / BK;
+        T.kb1 = lim < T.kb1 ? lim : T.kb1;
+    } else if (P.causal == kCausalKFromM) {
+        T.kb0 = m0 / BK;
+    }
+    if (T.kb0 >= T.kb1) T.skip = true;
+    return T;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(kThreads, 1)
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params P) {
+    constexpr uint32_t A_BYTES = BM * BK * 2;
+    constexpr uint32_t B_BYTES = BN * BK * 2;
+    constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B atoms
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* tfull = bars + 2 * STAGES;
+    uint64_t* tempty = bars + 2 * STAGES + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(smem_u32(&full[s]), 1);
+            mbar_init(smem_u32(&empty[s]), 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(smem_u32(&tfull[a]), 1);
+            mbar_init(smem_u32(&tempty[a]), 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(2 * BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===== TMA producer =====
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+                const Tile T = decode(P, t, BN);
+                if (T.skip) continue;
+                for (int kb = T.kb0; kb < T.kb1; ++kb) {
+                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_expect_tx(fb, STAGE_BYTES);
+                    const uint32_t a_dst = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b_dst = smem_u32(sB + stage * B_BYTES);
+                    const int k0 = kb * BK;
+                    if (!P.a_mn) {
+                        tma_load_4d(a_dst, &tmA, fb, k0, T.tm * BM, T.z1, T.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BM / 64; ++j)
+                            tma_load_4d(a_dst + j * (64 * BK * 2), &tmA, fb, T.tm * BM + j * 64, k0, T.z1, T.z2);
+                    }
+                    if (!P.b_mn) {
+                        tma_load_4d(b_dst, &tmB, fb, k0, T.tn * BN, T.z1, T.z2);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_4d(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===== MMA issuer =====
+            const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(P.a_mn) << 15) |
+                                   (uint32_t(P.b_mn) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+            // K-major: rows of 128 B, 8-row atoms 1024 B apart; K step of 16 = +32 B.
+            // MN-major: 64-element (128 B) chunks BK rows deep (LBO = 64*BK*2 B apart), 8-row
+            // K groups 1024 B apart; K step of 16 = +2048 B.
+            const uint32_t a_lbo = P.a_mn ? 64 * BK * 2 : 16, a_sbo = 1024, a_kstep = P.a_mn ? 2048 : 32;
+            const uint32_t b_lbo = P.b_mn ? 64 * BK * 2 : 16, b_sbo = 1024, b_kstep = P.b_mn ? 2048 : 32;
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+                const Tile T = decode(P, t, BN);
+                if (T.skip) continue;
+                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = T.kb0; kb < T.kb1; ++kb) {
+                    mbar_wait(smem_u32(&full[stage]), phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int k = 0; k < BK / 16; ++k) {
+                        const uint64_t ad = smem_desc(a_addr + k * a_kstep, a_lbo, a_sbo);
+                        const uint64_t bd = smem_desc(b_addr + k * b_kstep, b_lbo, b_sbo);
+                        tc_mma(d_tmem, ad, bd, idesc, (kb > T.kb0 || k > 0) ? 1u : 0u);
+                    }
+                    tc_commit(smem_u32(&empty[stage]));
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(smem_u32(&tfull[acc]));
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ===== epilogue =====
+        const int q = warp & 3;  // TMEM lane quarter
+        const int r = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
+            const Tile T = decode(P, t, BN);
+            if (T.skip) continue;
+            mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+            tc_fence_after();
+            const int m = T.tm * BM + r;
+            const bool row_ok = m < P.M;
+            const long long c_off = (long long)T.z1 * P.c_s1 + (long long)T.z2 * P.c_s2 + (long long)m * P.ldc;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                float v[32];
+                tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, v);
+                const int n0 = T.tn * BN + c * 32;
+                if (!row_ok || n0 >= P.N) continue;
+                const bool full_chunk = n0 + 32 <= P.N;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] *= P.alpha;
+                if (P.beta != 0.f) {
+                    if (P.c_f32) {
+                        const float* cp = static_cast<const float*>(P.C) + c_off + n0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (full_chunk || n0 + j < P.N) v[j] += P.beta * cp[j];
+                    } else {
+                        const uint16_t* cp = static_cast<const uint16_t*>(P.C) + c_off + n0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (full_chunk || n0 + j < P.N) v[j] += P.beta * bf16_bits_to_f32(cp[j]);
+                    }
+                }
+                if (P.epi & kEpiBias) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (!full_chunk && n0 + j >= P.N) break;
+                        v[j] += P.bias_f32 ? static_cast<const float*>(P.bias)[n0 + j]
+                                           : bf16_bits_to_f32(static_cast<const uint16_t*>(P.bias)[n0 + j]);
+                    }
+                }
+                if (P.epi & kEpiAux) {
+                    uint16_t* ap = P.aux + (long long)T.z1 * P.aux_s1 + (long long)T.z2 * P.aux_s2 +
+                                   (long long)m * P.ld_aux + n0;
+                    if (full_chunk && P.vec_aux) {
+                        uint4* a4 = reinterpret_cast<uint4*>(ap);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            a4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
+                                               pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                    } else {
+                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) ap[j] = (uint16_t)f32_to_bf16_bits(v[j]);
+                    }
+                }
+                if (P.epi & kEpiGelu) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+                }
+                if (P.epi & kEpiResidual) {
+                    const uint16_t* rp = P.res + (long long)T.z1 * P.res_s1 + (long long)T.z2 * P.res_s2 +
+                                         (long long)m * P.ld_res + n0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (full_chunk || n0 + j < P.N) v[j] += bf16_bits_to_f32(rp[j]);
+                }
+                if (P.c_f32) {
+                    float* cp = static_cast<float*>(P.C) + c_off + n0;
+                    if (full_chunk && P.vec_c) {
+                        float4* c4 = reinterpret_cast<float4*>(cp);
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) c4[w] = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+                    } else {
+                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) cp[j] = v[j];
+                    }
+                } else {
+                    uint16_t* cp = static_cast<uint16_t*>(P.C) + c_off + n0;
+                    if (full_chunk && P.vec_c) {
+                        uint4* c4 = reinterpret_cast<uint4*>(cp);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            c4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
+                                               pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                    } else {
+                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) cp[j] = (uint16_t)f32_to_bf16_bits(v[j]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------------------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// 4-D map over a bf16 operand: dims {inner, outer, b1, b2} with element strides.
+static bool make_map(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld,
+                     int b1, long long s1, int b2, long long s2, int box_inner, int box_outer) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    const long long plane = ld * outer;
+    if (b1 <= 1 || s1 == 0) s1 = plane;
+    if (b2 <= 1 || s2 == 0) s2 = s1 * (b1 > 0 ? b1 : 1);
+    cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(b1 > 0 ? b1 : 1), (cuuint64_t)(b2 > 0 ? b2 : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(s1 * 2), (cuuint64_t)(s2 * 2)};
+    cuuint32_t box[4] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, int STAGES>
+static size_t smem_bytes() {
+    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const Params& P, int grid,
+                              cudaStream_t stream) {
+    const size_t sm = smem_bytes<BN, STAGES>();
+    static bool configured = false;
+    if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e != cudaSuccess) return e;
+        configured = true;
+    }
+    gemm_kernel<BN, STAGES><<<grid, kThreads, sm, stream>>>(a, b, P);
+    return cudaGetLastError();
+}
+
+cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
+    if (g.K % 8 != 0) return cudaErrorInvalidValue;  // TMA: 16-byte strides
+    int BN = g.block_n;
+    if (BN == 0) BN = g.N >= 256 ? 256 : (g.N > 64 ? 128 : 64);
+    if (BN != 256 && BN != 128 && BN != 64) return cudaErrorInvalidValue;
+    Params P{};
+    P.M = (int)g.M;
+    P.N = (int)g.N;
+    P.K = (int)g.K;
+    P.batch1 = g.batch1 > 0 ? g.batch1 : 1;
+    P.batch2 = g.batch2 > 0 ? g.batch2 : 1;
+    P.tiles_m = (P.M + BM - 1) / BM;
+    P.tiles_n = (P.N + BN - 1) / BN;
+    P.num_tiles = P.tiles_m * P.tiles_n * P.batch1 * P.batch2;
+    P.k_blocks = (P.K + BK - 1) / BK;
+    P.a_mn = g.a_mn_major;
+    P.b_mn = g.b_mn_major;
+    P.C = g.C;
+    P.c_f32 = g.c_f32;
+    P.ldc = g.ldc;
+    P.c_s1 = g.c_s1;
+    P.c_s2 = g.c_s2;
+    P.bias = g.bias;
+    P.bias_f32 = g.bias_f32;
+    P.res = static_cast<const uint16_t*>(g.residual);
+    P.ld_res = g.ld_res;
+    P.res_s1 = g.res_s1;
+    P.res_s2 = g.res_s2;
+    P.aux = static_cast<uint16_t*>(g.aux);
+    P.ld_aux = g.ld_aux;
+    P.aux_s1 = g.aux_s1;
+    P.aux_s2 = g.aux_s2;
+    P.alpha = g.alpha;
+    P.beta = g.beta;
+    P.epi = g.epilogue;
+    P.causal = g.causal;
+    {
+        const long long ce = g.c_f32 ? 4 : 2, align = 16 / ce;
+        P.vec_c = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % align == 0 && g.c_s1 % align == 0 &&
+                  g.c_s2 % align == 0;
+        P.vec_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
+                    g.aux_s2 % 8 == 0;
+    }
+
+    CUtensorMap ma, mb;
+    const bool ok_a = g.a_mn_major
+                          ? make_map(&ma, g.A, g.M, g.K, g.lda, P.batch1, g.a_s1, P.batch2, g.a_s2, 64, 64)
+                          : make_map(&ma, g.A, g.K, g.M, g.lda, P.batch1, g.a_s1, P.batch2, g.a_s2, 64, BM);
+    const bool ok_b = g.b_mn_major
+                          ? make_map(&mb, g.B, g.N, g.K, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, 64)
+                          : make_map(&mb, g.B, g.K, g.N, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, BN);
+    if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+    int grid = P.num_tiles < kNumSMs ? P.num_tiles : kNumSMs;
+    if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+    if (BN == 256) return launch_cfg<256, 4>(ma, mb, P, grid, stream);
+    if (BN == 128) return launch_cfg<128, 6>(ma, mb, P, grid, stream);
+    return launch_cfg<64, 8>(ma, mb, P, grid, stream);
+}
+
+}  // namespace gemm
+}  // namespace ah
