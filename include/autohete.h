@@ -133,6 +133,60 @@ typedef struct ah_gemm_desc {
 
 int ah_gemm_bf16(const ah_gemm_desc* desc, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * Training executor: one GPT iteration = hetsim::build_iteration_ops(profile, strategy, k)
+ * (proj/core/src/simulator.cpp:91-229) executed on B200 in the per-lane order of
+ * hetsim::run(..., priority_sched) (simulator.cpp:263-596). The planner step is
+ * hetsim::solve + fine_tune_prefetch (proj/core/src/planner.cpp:37-153) on a profile built
+ * from the real block shape and the rates given here (measured on the box by the caller).
+ * --------------------------------------------------------------------------------------- */
+typedef struct ah_trainer_config {
+    int32_t num_blocks, hidden, heads, seq_len, batch, vocab;
+    /* strategy: c_hat/p_hat/o_hat >= 0 forces it; any < 0 => planner decides */
+    int32_t c_hat, p_hat, o_hat;
+    const int32_t* prefetch_lookahead; /* nullable; L entries when forcing a strategy */
+    int32_t priority_sched;            /* 1: PS order (paper §3.3), 0: FIFO */
+    int32_t fine_tune;                 /* run fine_tune_prefetch after solve */
+    int64_t gpu_mem_budget, cpu_mem_budget; /* planner budgets, bytes */
+    double gpu_flops, h2d_bw, d2h_bw, cpu_adam_rate, gpu_adam_rate; /* HardwareSpec rates */
+    ah_adam_hparams adam;
+    uint64_t seed;
+    int32_t cpu_threads; /* CPU Adam threads, <= 0 = all */
+} ah_trainer_config;
+
+typedef struct ah_trainer_stats {
+    int32_t c_hat, p_hat, o_hat;
+    double activation_coef;       /* real bytes of a block's activations / (2*b*s*h) */
+    int64_t m_p, m_gc;            /* per-block params, constant GPU residue (bytes) */
+    int64_t modeled_peak_bytes;   /* Eq.(1) for the chosen strategy */
+    int64_t simulated_peak_bytes; /* hetsim::run peak */
+    int64_t pool_peak_bytes;      /* measured: stream-ordered pool high watermark */
+    int64_t static_bytes;         /* measured: persistent device allocations */
+    double sim_steady_s;          /* hetsim::run steady-state iteration time */
+    double lane_busy_ms[4];       /* compute, h2d, d2h, cpu: summed op time since reset */
+    int32_t lane_ops[4];
+    int64_t h2d_bytes, d2h_bytes; /* parameter prefetch / grad offload bytes per iteration */
+    int32_t kernels_per_iter;     /* our kernel launches per iteration */
+} ah_trainer_stats;
+
+int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);
+int ah_trainer_destroy(void* trainer);
+/* Async: enqueue one iteration; inputs are B*s int32 on host (or device if on_device). */
+int ah_trainer_submit(void* trainer, const int32_t* tokens, const int32_t* targets, int32_t on_device);
+/* Wait for all submitted iterations; *loss = mean loss of the last one. */
+int ah_trainer_drain(void* trainer, float* loss);
+/* Synchronous e2e step: H2D inputs, iteration, D2H loss. */
+int ah_trainer_step(void* trainer, const int32_t* tokens, const int32_t* targets, float* loss);
+int ah_trainer_stats_get(void* trainer, ah_trainer_stats* out);
+int ah_trainer_reset_stats(void* trainer);
+/* Per-lane op order of one steady-state iteration as "LANE:OP_block" tokens. */
+int ah_trainer_schedule(void* trainer, char* buf, size_t cap);
+/* fp32 master parameters of block b (1..L), 0 = token embedding, -1 = positions,
+ * -2 = final LayerNorm; n = element count written to out (host). */
+int ah_trainer_read_master(void* trainer, int32_t block, float* out, size_t n);
+int64_t ah_trainer_master_size(void* trainer, int32_t block);
+int ah_trainer_trace(void* trainer, char* buf, size_t cap); /* Chrome trace JSON, measured */
+
 #ifdef __cplusplus
 }
 #endif

@@ -116,3 +116,43 @@ def _declare_extra(L):
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res
+
+
+class TrainerConfig(C.Structure):
+    _fields_ = [
+        ("num_blocks", C.c_int32), ("hidden", C.c_int32), ("heads", C.c_int32), ("seq_len", C.c_int32),
+        ("batch", C.c_int32), ("vocab", C.c_int32),
+        ("c_hat", C.c_int32), ("p_hat", C.c_int32), ("o_hat", C.c_int32),
+        ("prefetch_lookahead", C.POINTER(C.c_int32)),
+        ("priority_sched", C.c_int32), ("fine_tune", C.c_int32),
+        ("gpu_mem_budget", C.c_int64), ("cpu_mem_budget", C.c_int64),
+        ("gpu_flops", C.c_double), ("h2d_bw", C.c_double), ("d2h_bw", C.c_double),
+        ("cpu_adam_rate", C.c_double), ("gpu_adam_rate", C.c_double),
+        ("adam", AdamHParams), ("seed", C.c_uint64), ("cpu_threads", C.c_int32),
+    ]
+
+
+class TrainerStats(C.Structure):
+    _fields_ = [
+        ("c_hat", C.c_int32), ("p_hat", C.c_int32), ("o_hat", C.c_int32),
+        ("activation_coef", C.c_double), ("m_p", C.c_int64), ("m_gc", C.c_int64),
+        ("modeled_peak_bytes", C.c_int64), ("simulated_peak_bytes", C.c_int64),
+        ("pool_peak_bytes", C.c_int64), ("static_bytes", C.c_int64), ("sim_steady_s", C.c_double),
+        ("lane_busy_ms", C.c_double * 4), ("lane_ops", C.c_int32 * 4),
+        ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("kernels_per_iter", C.c_int32),
+    ]
+
+
+_EXTRA_SIGS.update({
+    "ah_trainer_create": ([C.POINTER(TrainerConfig), C.POINTER(C.c_void_p)], C.c_int),
+    "ah_trainer_destroy": ([C.c_void_p], C.c_int),
+    "ah_trainer_submit": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32], C.c_int),
+    "ah_trainer_drain": ([C.c_void_p, C.POINTER(C.c_float)], C.c_int),
+    "ah_trainer_step": ([C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_float)], C.c_int),
+    "ah_trainer_stats_get": ([C.c_void_p, C.POINTER(TrainerStats)], C.c_int),
+    "ah_trainer_reset_stats": ([C.c_void_p], C.c_int),
+    "ah_trainer_schedule": ([C.c_void_p, C.c_char_p, C.c_size_t], C.c_int),
+    "ah_trainer_read_master": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
+    "ah_trainer_master_size": ([C.c_void_p, C.c_int32], C.c_int64),
+    "ah_trainer_trace": ([C.c_void_p, C.c_char_p, C.c_size_t], C.c_int),
+})

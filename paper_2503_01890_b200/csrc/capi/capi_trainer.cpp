@@ -1,0 +1,117 @@
+// extern "C" boundary of the training executor (include/autohete.h, "Training executor").
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "autohete.h"
+#include "../runtime/executor.h"
+#include "capi_util.h"
+#include "hetsim/planner.hpp"
+#include "hetsim/simulator.hpp"
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return AH_OK;
+    } catch (const hetsim::InfeasibleError& e) {
+        return ah::set_error(AH_ERR_INFEASIBLE, e.what());
+    } catch (const hetsim::MemoryExceededError& e) {
+        return ah::set_error(AH_ERR_MEMORY, e.what());
+    } catch (const std::invalid_argument& e) {
+        return ah::set_error(AH_ERR_INVALID, e.what());
+    } catch (const std::exception& e) {
+        const std::string w = e.what();
+        return ah::set_error(w.find("CUDA") != std::string::npos || w.find("cuda") != std::string::npos ? AH_ERR_CUDA
+                                                                                                         : AH_ERR_INTERNAL,
+                             w);
+    }
+}
+
+ah::Trainer* T(void* p) { return static_cast<ah::Trainer*>(p); }
+
+int copy_out(const std::string& s, char* buf, size_t cap) {
+    if (!buf || cap == 0) return (int)s.size() + 1;
+    const size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+    return (int)s.size() + 1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int ah_trainer_create(const ah_trainer_config* cfg, void** out) {
+    if (!cfg || !out) return ah::set_error(AH_ERR_INVALID, "ah_trainer_create: null argument");
+    return guarded([&] { *out = new ah::Trainer(*cfg); });
+}
+
+int ah_trainer_destroy(void* tr) {
+    return guarded([&] { delete T(tr); });
+}
+
+int ah_trainer_submit(void* tr, const int32_t* tokens, const int32_t* targets, int32_t on_device) {
+    if (!tr || !tokens || !targets) return ah::set_error(AH_ERR_INVALID, "ah_trainer_submit: null argument");
+    return guarded([&] { T(tr)->submit(tokens, targets, on_device != 0); });
+}
+
+int ah_trainer_drain(void* tr, float* loss) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "ah_trainer_drain: null trainer");
+    return guarded([&] {
+        const float l = T(tr)->drain();
+        if (loss) *loss = l;
+    });
+}
+
+int ah_trainer_step(void* tr, const int32_t* tokens, const int32_t* targets, float* loss) {
+    if (!tr || !tokens || !targets) return ah::set_error(AH_ERR_INVALID, "ah_trainer_step: null argument");
+    return guarded([&] {
+        const float l = T(tr)->step(tokens, targets);
+        if (loss) *loss = l;
+    });
+}
+
+int ah_trainer_stats_get(void* tr, ah_trainer_stats* out) {
+    if (!tr || !out) return ah::set_error(AH_ERR_INVALID, "ah_trainer_stats_get: null argument");
+    return guarded([&] { T(tr)->stats(out); });
+}
+
+int ah_trainer_reset_stats(void* tr) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    return AH_OK;
+}
+
+int ah_trainer_schedule(void* tr, char* buf, size_t cap) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    std::string s;
+    const hetsim::SimResult& r = T(tr)->simulated();
+    for (const auto& op : r.trace) {
+        if (op.iter != 2) continue;
+        s += std::string(hetsim::stream_name(op.stream)) + ":" + hetsim::op_code(op.kind) + "_" +
+             std::to_string(op.block) + (op.backward_copy ? "b" : "") + " ";
+    }
+    return copy_out(s, buf, cap);
+}
+
+int ah_trainer_read_master(void* tr, int32_t block, float* out, size_t n) {
+    if (!tr || !out) return ah::set_error(AH_ERR_INVALID, "null argument");
+    return guarded([&] { T(tr)->read_master(block, out, n); });
+}
+
+int64_t ah_trainer_master_size(void* tr, int32_t block) {
+    if (!tr) return -1;
+    return (int64_t)T(tr)->master_size(block);
+}
+
+int ah_trainer_trace(void* tr, char* buf, size_t cap) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    std::string s;
+    const int rc = guarded([&] { s = T(tr)->trace_json(); });
+    if (rc != AH_OK) return rc;
+    return copy_out(s, buf, cap);
+}
+
+}  // extern "C"

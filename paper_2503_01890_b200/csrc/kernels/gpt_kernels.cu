@@ -1,0 +1,548 @@
+// Non-GEMM kernels of the GPT-2 block step (the Compute-lane work around the tcgen05 GEMMs
+// in OpKind::Forward / Backward / Recompute): embedding, LayerNorm fwd/bwd, causal softmax
+// fwd/bwd, GELU bwd, deterministic column reductions (bias / LN-affine / position grads),
+// fused cross-entropy fwd+bwd, deterministic token-embedding scatter.
+// All HBM-bound: 16-byte vector access, one warp per row where rows are reduced, fp32 math,
+// bf16 storage. Every reduction has a fixed order (no float atomics) so recompute and
+// offload plans reproduce bit-identical training state.
+#include "common.cuh"
+#include "gpt_kernels.h"
+
+namespace ah {
+namespace gpt {
+
+namespace {
+
+constexpr float kLnEps = 1e-5f;
+
+__device__ __forceinline__ void unpack8(const uint4& w, float (&f)[8]) {
+    const uint32_t a[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        f[2 * i] = bf16_bits_to_f32(a[i] & 0xffffu);
+        f[2 * i + 1] = bf16_bits_to_f32(a[i] >> 16);
+    }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+    return make_uint4(pack_bf16x2(f[0], f[1]), pack_bf16x2(f[2], f[3]), pack_bf16x2(f[4], f[5]),
+                      pack_bf16x2(f[6], f[7]));
+}
+__device__ __forceinline__ uint4 ldg16(const void* p) { return *reinterpret_cast<const uint4*>(p); }
+__device__ __forceinline__ void stg16(void* p, uint4 v) { *reinterpret_cast<uint4*>(p) = v; }
+
+// ---------------------------------------------------------------------------------------
+__global__ void embed_fwd_kernel(const int* __restrict__ tok, const uint16_t* __restrict__ wte,
+                                 const uint16_t* __restrict__ wpe, uint16_t* __restrict__ x, int T, int s, int h) {
+    const int t = blockIdx.x;
+    const int id = tok[t];
+    const int pos = t % s;
+    for (int c = threadIdx.x * 8; c < h; c += blockDim.x * 8) {
+        float a[8], b[8];
+        unpack8(ldg16(wte + (size_t)id * h + c), a);
+        unpack8(ldg16(wpe + (size_t)pos * h + c), b);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] += b[i];
+        stg16(x + (size_t)t * h + c, pack8(a));
+    }
+}
+
+// One warp per row. Three passes over the row (L1-resident) for an accurate variance.
+__global__ void ln_fwd_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
+                              const uint16_t* __restrict__ b, uint16_t* __restrict__ y, float* __restrict__ mean,
+                              float* __restrict__ rstd, int T, int h) {
+    const int warps = blockDim.x >> 5;
+    const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const uint16_t* xr = x + (size_t)row * h;
+    float s = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+        float f[8];
+        unpack8(ldg16(xr + c), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += f[i];
+    }
+    const float mu = warp_sum(s) / h;
+    float v = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+        float f[8];
+        unpack8(ldg16(xr + c), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v += (f[i] - mu) * (f[i] - mu);
+    }
+    const float rs = rsqrtf(warp_sum(v) / h + kLnEps);
+    for (int c = lane * 8; c < h; c += 256) {
+        float f[8], gg[8], bb[8];
+        unpack8(ldg16(xr + c), f);
+        unpack8(ldg16(g + c), gg);
+        unpack8(ldg16(b + c), bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = (f[i] - mu) * rs * gg[i] + bb[i];
+        stg16(y + (size_t)row * h + c, pack8(f));
+    }
+    if (lane == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+    }
+}
+
+// dx = rstd*(dy*g - mean(dy*g) - xhat*mean(dy*g*xhat)) (+ dres). Per-CTA partial sums of
+// dg = sum(dy*xhat), db = sum(dy) over the CTA's rows go to part[cta][2h] (fixed order).
+__global__ void ln_bwd_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                              const float* __restrict__ mean, const float* __restrict__ rstd,
+                              const uint16_t* __restrict__ g, const uint16_t* dres, uint16_t* dx,
+                              float* __restrict__ part, int T, int h, int rows_per_cta) {
+    extern __shared__ float acc[];  // [warps][2h]
+    const int warps = blockDim.x >> 5;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float* my = acc + (size_t)w * 2 * h;
+    for (int c = lane; c < 2 * h; c += 32) my[c] = 0.f;
+    __syncwarp();
+    const int r0 = blockIdx.x * rows_per_cta;
+    const int r1 = min(T, r0 + rows_per_cta);
+    for (int row = r0 + w; row < r1; row += warps) {
+        const uint16_t* xr = x + (size_t)row * h;
+        const uint16_t* dyr = dy + (size_t)row * h;
+        const float mu = mean[row], rs = rstd[row];
+        float s1 = 0.f, s2 = 0.f;
+        for (int c = lane * 8; c < h; c += 256) {
+            float xf[8], df[8], gf[8];
+            unpack8(ldg16(xr + c), xf);
+            unpack8(ldg16(dyr + c), df);
+            unpack8(ldg16(g + c), gf);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = (xf[i] - mu) * rs;
+                const float dg = df[i] * gf[i];
+                s1 += dg;
+                s2 += dg * xh;
+                my[c + i] += df[i] * xh;
+                my[h + c + i] += df[i];
+            }
+        }
+        s1 = warp_sum(s1) / h;
+        s2 = warp_sum(s2) / h;
+        for (int c = lane * 8; c < h; c += 256) {
+            float xf[8], df[8], gf[8], rf[8];
+            unpack8(ldg16(xr + c), xf);
+            unpack8(ldg16(dyr + c), df);
+            unpack8(ldg16(g + c), gf);
+            if (dres) unpack8(ldg16(dres + (size_t)row * h + c), rf);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float xh = (xf[i] - mu) * rs;
+                float d = rs * (df[i] * gf[i] - s1 - xh * s2);
+                if (dres) d += rf[i];
+                xf[i] = d;
+            }
+            stg16(dx + (size_t)row * h + c, pack8(xf));
+        }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < 2 * h; c += blockDim.x) {
+        float t = 0.f;
+        for (int q = 0; q < warps; ++q) t += acc[(size_t)q * 2 * h + c];
+        part[(size_t)blockIdx.x * 2 * h + c] = t;
+    }
+}
+
+// part[r][n] = sum over rows [r*rows, (r+1)*rows) of X[row][n]; 8 columns per thread.
+__global__ void colsum_partial_kernel(const uint16_t* __restrict__ X, int T, int N, int ldx, int rows,
+                                      float* __restrict__ part) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= N) return;
+    const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0; r < r1; ++r) {
+        float f[8];
+        unpack8(ldg16(X + (size_t)r * ldx + c), f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] += f[i];
+    }
+    float* dst = part + (size_t)blockIdx.y * N + c;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[i] = a[i];
+}
+
+// out[n] (bf16 or fp32) = sum_r part[r][n], r ascending.
+__global__ void colsum_finish_kernel(const float* __restrict__ part, int R, int N, void* out, int out_f32,
+                                     float* out2_f32) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    float t = 0.f;
+    for (int r = 0; r < R; ++r) t += part[(size_t)r * N + n];
+    if (out_f32)
+        static_cast<float*>(out)[n] = t;
+    else
+        static_cast<uint16_t*>(out)[n] = (uint16_t)f32_to_bf16_bits(t);
+    if (out2_f32) out2_f32[n] = t;
+}
+
+// Causal softmax over rows of S (already scaled). One warp per row i of matrix z:
+// P[j] = exp(S[j]-max)/sum for j <= i, 0 for i < j < end of i's 128-row tile.
+__global__ void softmax_fwd_kernel(const float* __restrict__ S, uint16_t* __restrict__ P, long long rows, int s) {
+    const long long gr = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (gr >= rows) return;
+    const int i = (int)(gr % s);
+    const float* sr = S + gr * s;
+    uint16_t* pr = P + gr * s;
+    float mx = -INFINITY;
+    for (int j = lane; j <= i; j += 32) mx = fmaxf(mx, sr[j]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    float sum = 0.f;
+    for (int j = lane; j <= i; j += 32) sum += __expf(sr[j] - mx);
+    const float inv = 1.f / warp_sum(sum);
+    const int end = min(s, (i / 128 + 1) * 128);
+    for (int j = lane; j < end; j += 32)
+        pr[j] = (uint16_t)(j <= i ? f32_to_bf16_bits(__expf(sr[j] - mx) * inv) : 0u);
+}
+
+// dS[j] = P[j] * (dP[j] - sum_k P[k] dP[k]) for j <= i, 0 up to the tile end.
+__global__ void softmax_bwd_kernel(const uint16_t* __restrict__ P, const float* __restrict__ dP,
+                                   uint16_t* __restrict__ dS, long long rows, int s) {
+    const long long gr = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (gr >= rows) return;
+    const int i = (int)(gr % s);
+    const uint16_t* pr = P + gr * s;
+    const float* dr = dP + gr * s;
+    uint16_t* out = dS + gr * s;
+    float d = 0.f;
+    for (int j = lane; j <= i; j += 32) d += bf16_bits_to_f32(pr[j]) * dr[j];
+    d = warp_sum(d);
+    const int end = min(s, (i / 128 + 1) * 128);
+    for (int j = lane; j < end; j += 32) {
+        float v = 0.f;
+        if (j <= i) v = bf16_bits_to_f32(pr[j]) * (dr[j] - d);
+        out[j] = (uint16_t)f32_to_bf16_bits(v);
+    }
+}
+
+__device__ __forceinline__ float gelu_grad(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float u = k0 * (x + k1 * x * x * x);
+    const float th = tanhf(u);
+    const float du = k0 * (1.f + 3.f * k1 * x * x);
+    return 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * du;
+}
+
+__global__ void gelu_bwd_kernel(const uint16_t* dgelu, const uint16_t* __restrict__ pre, uint16_t* dpre, size_t n8) {
+    for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n8; j += (size_t)gridDim.x * blockDim.x) {
+        float d[8], p[8];
+        unpack8(ldg16(dgelu + j * 8), d);
+        unpack8(ldg16(pre + j * 8), p);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] *= gelu_grad(p[i]);
+        stg16(dpre + j * 8, pack8(d));
+    }
+}
+
+// Cross-entropy over V real columns of a row of logits (ld = padded V); writes per-row
+// loss and, in place, dlogits = (softmax - onehot) * dscale (0 in padding columns).
+__global__ void ce_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__ loss, int V, int ld,
+                          float dscale) {
+    __shared__ float red[32];
+    const int row = blockIdx.x;
+    uint16_t* lr = logits + (size_t)row * ld;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    float mx = -INFINITY;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) mx = fmaxf(mx, bf16_bits_to_f32(lr[j]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) red[w] = mx;
+    __syncthreads();
+    mx = red[0];
+    for (int q = 1; q < nw; ++q) mx = fmaxf(mx, red[q]);
+    __syncthreads();
+    float sum = 0.f;
+    for (int j = threadIdx.x; j < V; j += blockDim.x) sum += __expf(bf16_bits_to_f32(lr[j]) - mx);
+    sum = warp_sum(sum);
+    if (lane == 0) red[w] = sum;
+    __syncthreads();
+    sum = 0.f;
+    for (int q = 0; q < nw; ++q) sum += red[q];
+    const int t = tgt[row];
+    const float lse = mx + __logf(sum);
+    const float tl = bf16_bits_to_f32(lr[t]);
+    __syncthreads();
+    if (threadIdx.x == 0) loss[row] = lse - tl;
+    const float inv = 1.f / sum;
+    for (int j = threadIdx.x; j < ld; j += blockDim.x) {
+        float d = 0.f;
+        if (j < V) d = (__expf(bf16_bits_to_f32(lr[j]) - mx) * inv - (j == t ? 1.f : 0.f)) * dscale;
+        lr[j] = (uint16_t)f32_to_bf16_bits(d);
+    }
+}
+
+// dwte[v] += sum over positions of v (ascending order) of dx[pos]; one CTA per distinct token.
+__global__ void embed_bwd_tok_kernel(const uint16_t* __restrict__ dx, const int* __restrict__ uniq,
+                                     const int* __restrict__ offs, const int* __restrict__ pos, float* dwte, int h) {
+    const int u = blockIdx.x;
+    const int v = uniq[u];
+    for (int c = threadIdx.x * 8; c < h; c += blockDim.x * 8) {
+        float a[8];
+        float* dst = dwte + (size_t)v * h + c;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = dst[i];
+        for (int q = offs[u]; q < offs[u + 1]; ++q) {
+            float f[8];
+            unpack8(ldg16(dx + (size_t)pos[q] * h + c), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] += f[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = a[i];
+    }
+}
+
+// dwpe[p] = sum_b dx[b*s + p]  (fp32 out)
+__global__ void embed_bwd_pos_kernel(const uint16_t* __restrict__ dx, float* __restrict__ dwpe, int B, int s, int h) {
+    const int p = blockIdx.x;
+    for (int c = threadIdx.x * 8; c < h; c += blockDim.x * 8) {
+        float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int b = 0; b < B; ++b) {
+            float f[8];
+            unpack8(ldg16(dx + ((size_t)b * s + p) * h + c), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] += f[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dwpe[(size_t)p * h + c + i] = a[i];
+    }
+}
+
+__global__ void f32_to_bf16_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst, size_t n) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+        dst[i] = (uint16_t)f32_to_bf16_bits(src[i]);
+}
+
+__global__ void loss_sum_kernel(const float* __restrict__ loss, int T, float* out) {
+    __shared__ float red[32];
+    float s = 0.f;
+    for (int i = threadIdx.x; i < T; i += blockDim.x) s += loss[i];
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q];
+        *out = t / T;
+    }
+}
+
+}  // namespace
+
+cudaError_t embed_fwd(const int* tok, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int T, int s, int h,
+                      cudaStream_t st) {
+    embed_fwd_kernel<<<T, 256, 0, st>>>(tok, wte, wpe, x, T, s, h);
+    return cudaGetLastError();
+}
+
+cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean, float* rstd,
+                   int T, int h, cudaStream_t st) {
+    ln_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T, h);
+    return cudaGetLastError();
+}
+
+int ln_bwd_ctas(int T) { return T < 592 ? T : 592; }
+
+static int ln_bwd_warps(int h) {
+    const int w = (200 * 1024) / (2 * h * 4);
+    return w < 1 ? 1 : (w > 4 ? 4 : w);
+}
+
+cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
+                   const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st) {
+    const int ctas = ln_bwd_ctas(T);
+    const int rows = (T + ctas - 1) / ctas;
+    const int warps = ln_bwd_warps(h);
+    const size_t sm = (size_t)warps * 2 * h * sizeof(float);
+    static bool cfg = false;
+    if (!cfg) {
+        cudaFuncSetAttribute(ln_bwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cfg = true;
+    }
+    ln_bwd_kernel<<<ctas, warps * 32, sm, st>>>(dy, x, mean, rstd, g, dres, dx, part, T, h, rows);
+    colsum_finish_kernel<<<(2 * h + 255) / 256, 256, 0, st>>>(part, ctas, 2 * h, dgdb, 0, nullptr);
+    return cudaGetLastError();
+}
+
+int colsum_rows(int T) { return T >= 4096 ? 64 : (T >= 256 ? 16 : 1); }
+
+cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st) {
+    const int R = colsum_rows(T);
+    const int rows = (T + R - 1) / R;
+    dim3 grid((N / 8 + 127) / 128, R);
+    colsum_partial_kernel<<<grid, 128, 0, st>>>(X, T, N, ldx, rows, part);
+    colsum_finish_kernel<<<(N + 255) / 256, 256, 0, st>>>(part, R, N, out, out_f32, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st) {
+    softmax_fwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(S, P, rows, s);
+    return cudaGetLastError();
+}
+
+cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st) {
+    softmax_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(P, dP, dS, rows, s);
+    return cudaGetLastError();
+}
+
+cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre, size_t n, cudaStream_t st) {
+    const size_t n8 = n / 8;
+    gelu_bwd_kernel<<<148 * 8, 256, 0, st>>>(dgelu, pre, dpre, n8);
+    return cudaGetLastError();
+}
+
+cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
+                          cudaStream_t st) {
+    ce_kernel<<<T, 512, 0, st>>>(logits, tgt, loss, V, ld, dscale);
+    return cudaGetLastError();
+}
+
+cudaError_t embed_bwd_tok(const uint16_t* dx, const int* uniq, const int* offs, const int* pos, int n_uniq,
+                          float* dwte, int h, cudaStream_t st) {
+    if (n_uniq > 0) embed_bwd_tok_kernel<<<n_uniq, 256, 0, st>>>(dx, uniq, offs, pos, dwte, h);
+    return cudaGetLastError();
+}
+
+cudaError_t embed_bwd_pos(const uint16_t* dx, float* dwpe, int B, int s, int h, cudaStream_t st) {
+    embed_bwd_pos_kernel<<<s, 256, 0, st>>>(dx, dwpe, B, s, h);
+    return cudaGetLastError();
+}
+
+cudaError_t f32_to_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st) {
+    f32_to_bf16_kernel<<<148 * 8, 256, 0, st>>>(src, dst, n);
+    return cudaGetLastError();
+}
+
+cudaError_t mean_loss(const float* loss, int T, float* out, cudaStream_t st) {
+    loss_sum_kernel<<<1, 1024, 0, st>>>(loss, T, out);
+    return cudaGetLastError();
+}
+
+}  // namespace gpt
+}  // namespace ah
+
+namespace ah {
+namespace gpt {
+namespace {
+__device__ __forceinline__ unsigned long long splitmix(unsigned long long x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__global__ void init_normal_kernel(float* p, size_t n, unsigned long long seed, float mean, float std) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long r = splitmix(seed ^ splitmix(i));
+        const float u1 = ((r >> 40) + 1) * (1.0f / 16777217.0f);
+        const float u2 = ((r & 0xFFFFFFull)) * (1.0f / 16777216.0f);
+        p[i] = mean + std * sqrtf(-2.f * logf(u1)) * cospif(2.f * u2);
+    }
+}
+__global__ void fill_kernel(float* p, size_t n, float v) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+}  // namespace
+cudaError_t init_normal(float* p, size_t n, unsigned long long seed, float mean, float std, cudaStream_t st) {
+    init_normal_kernel<<<148 * 8, 256, 0, st>>>(p, n, seed, mean, std);
+    return cudaGetLastError();
+}
+cudaError_t fill_f32(float* p, size_t n, float v, cudaStream_t st) {
+    fill_kernel<<<148 * 8, 256, 0, st>>>(p, n, v);
+    return cudaGetLastError();
+}
+}  // namespace gpt
+}  // namespace ah
+
+namespace ah {
+namespace gpt {
+namespace {
+__global__ void __launch_bounds__(1024) token_index_kernel(const int* __restrict__ tok, int T, int n2, int* uniq,
+                                                            int* offs, int* pos, int* n_uniq) {
+    extern __shared__ unsigned long long keys[];  // n2 keys, then n2 ints of scan space
+    int* flag = reinterpret_cast<int*>(keys + n2);
+    for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        keys[i] = i < T ? ((unsigned long long)(unsigned)tok[i] << 32) | (unsigned)i : ~0ull;
+    __syncthreads();
+    for (int k = 2; k <= n2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    const unsigned long long a = keys[i], b = keys[ixj];
+                    if ((a > b) == up) {
+                        keys[i] = b;
+                        keys[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = threadIdx.x; i < T; i += blockDim.x)
+        flag[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {  // serial scan over T <= 16384 flags (tiny)
+        int u = 0;
+        for (int i = 0; i < T; ++i) {
+            if (flag[i]) {
+                uniq[u] = (int)(keys[i] >> 32);
+                offs[u] = i;
+                ++u;
+            }
+        }
+        offs[u] = T;
+        *n_uniq = u;
+    }
+    for (int i = threadIdx.x; i < T; i += blockDim.x) pos[i] = (int)(keys[i] & 0xffffffffu);
+}
+
+__global__ void embed_bwd_tok_dev_kernel(const uint16_t* __restrict__ dx, const int* __restrict__ uniq,
+                                         const int* __restrict__ offs, const int* __restrict__ pos,
+                                         const int* __restrict__ n_uniq, float* dwte, int h) {
+    const int u = blockIdx.x;
+    if (u >= *n_uniq) return;
+    const int v = uniq[u];
+    for (int c = threadIdx.x * 8; c < h; c += blockDim.x * 8) {
+        float a[8];
+        float* dst = dwte + (size_t)v * h + c;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = dst[i];
+        for (int q = offs[u]; q < offs[u + 1]; ++q) {
+            float f[8];
+            unpack8(ldg16(dx + (size_t)pos[q] * h + c), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] += f[i];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dst[i] = a[i];
+    }
+}
+}  // namespace
+
+cudaError_t token_index(const int* tok, int T, int* uniq, int* offs, int* pos, int* n_uniq, cudaStream_t st) {
+    int n2 = 1;
+    while (n2 < T) n2 <<= 1;
+    if (n2 > 16384) return cudaErrorInvalidValue;
+    const size_t sm = (size_t)n2 * 8 + (size_t)n2 * 4;
+    static bool cfg = false;
+    if (!cfg) {
+        cudaFuncSetAttribute(token_index_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cfg = true;
+    }
+    token_index_kernel<<<1, 1024, sm, st>>>(tok, T, n2, uniq, offs, pos, n_uniq);
+    return cudaGetLastError();
+}
+
+cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* offs, const int* pos,
+                              const int* n_uniq, int T, float* dwte, int h, cudaStream_t st) {
+    embed_bwd_tok_dev_kernel<<<T, 256, 0, st>>>(dx, uniq, offs, pos, n_uniq, dwte, h);
+    return cudaGetLastError();
+}
+}  // namespace gpt
+}  // namespace ah

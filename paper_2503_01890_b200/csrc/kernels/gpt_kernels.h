@@ -1,0 +1,54 @@
+// Launchers for the non-GEMM GPT kernels (gpt_kernels.cu). bf16 tensors are uint16_t*.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ah {
+namespace gpt {
+
+cudaError_t embed_fwd(const int* tok, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int T, int s, int h,
+                      cudaStream_t st);
+cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean, float* rstd,
+                   int T, int h, cudaStream_t st);
+// dgdb: 2h contiguous bf16 = [dgamma | dbeta]; part: >= ln_bwd_ctas(T) * 2h floats.
+int ln_bwd_ctas(int T);
+cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
+                   const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st);
+// Column sums of X[T][N] (row stride ldx) -> out[N] (bf16 or fp32); part: >= colsum_rows(T)*N floats.
+int colsum_rows(int T);
+cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);
+cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
+cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);
+cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre, size_t n, cudaStream_t st);
+cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
+                          cudaStream_t st);
+cudaError_t embed_bwd_tok(const uint16_t* dx, const int* uniq, const int* offs, const int* pos, int n_uniq,
+                          float* dwte, int h, cudaStream_t st);
+cudaError_t embed_bwd_pos(const uint16_t* dx, float* dwpe, int B, int s, int h, cudaStream_t st);
+cudaError_t f32_to_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
+cudaError_t mean_loss(const float* loss, int T, float* out, cudaStream_t st);
+
+}  // namespace gpt
+}  // namespace ah
+
+namespace ah {
+namespace gpt {
+// Deterministic counter-based init: p[i] = mean + std * N(0,1)(seed, i).
+cudaError_t init_normal(float* p, size_t n, unsigned long long seed, float mean, float std, cudaStream_t st);
+cudaError_t fill_f32(float* p, size_t n, float v, cudaStream_t st);
+}  // namespace gpt
+}  // namespace ah
+
+namespace ah {
+namespace gpt {
+// Deterministic token -> positions index for the embedding backward, built on device:
+// sorts (token, position) pairs (single CTA bitonic sort, T <= 16384) and emits
+// uniq[n_uniq], offs[n_uniq + 1], pos[T] and *n_uniq. Buffers: ints of T, T+1, T, 1.
+cudaError_t token_index(const int* tok, int T, int* uniq, int* offs, int* pos, int* n_uniq, cudaStream_t st);
+// embedding scatter using the device-side count (grid = T, CTAs beyond n_uniq exit)
+cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* offs, const int* pos,
+                              const int* n_uniq, int T, float* dwte, int h, cudaStream_t st);
+}  // namespace gpt
+}  // namespace ah

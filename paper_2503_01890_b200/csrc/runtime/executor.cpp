@@ -1,0 +1,764 @@
+// B200 executor of the planned AutoHete iteration (see executor.h).
+#include "executor.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+
+#include "../kernels/gemm.h"
+#include "../kernels/gpt_kernels.h"
+#include "../kernels/kernels.h"
+#include "adam_scalars.h"
+#include "hetsim/costmodel.hpp"
+#include "hetsim/workload.hpp"
+
+namespace ah {
+
+void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uint16_t* g, uint16_t* p_bf16,
+              std::size_t n, float inv_scale, int nthreads);
+
+namespace {
+
+using hetsim::OpKind;
+using Clock = std::chrono::steady_clock;
+
+int lane_of(OpKind k) { return static_cast<int>(hetsim::stream_of(k)) - 1; }
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+AdamArgs adam_args(const ah_adam_hparams& hp, int step, float* p, float* m, float* v, const uint16_t* g,
+                   uint16_t* out, size_t n) {
+    ah_adam_hparams h = hp;
+    h.step = step;
+    const AdamConsts c = derive_adam_scalars(h);
+    AdamArgs a;
+    a.p = p;
+    a.m = m;
+    a.v = v;
+    a.g = g;
+    a.p_bf16 = out;
+    a.n = n;
+    a.decay = c.decay;
+    a.beta1 = c.beta1;
+    a.one_minus_beta1 = c.one_minus_beta1;
+    a.beta2 = c.beta2;
+    a.one_minus_beta2 = c.one_minus_beta2;
+    a.step_size = c.step_size;
+    a.inv_sqrt_bc2 = c.inv_sqrt_bc2;
+    a.eps = c.eps;
+    a.inv_scale = 1.f;
+    return a;
+}
+
+}  // namespace
+
+void Trainer::check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+cudaStream_t Trainer::stream_of(int lane) const {
+    return lane == kCompute ? s_compute_ : (lane == kH2D ? s_h2d_ : s_d2h_);
+}
+
+Trainer::Trainer(const ah_trainer_config& cfg) {
+    d_.L = cfg.num_blocks;
+    d_.h = cfg.hidden;
+    d_.nh = cfg.heads;
+    d_.hd = cfg.heads > 0 ? cfg.hidden / cfg.heads : 0;
+    d_.s = cfg.seq_len;
+    d_.B = cfg.batch;
+    d_.V = cfg.vocab;
+    d_.Vp = (int)round_up((size_t)cfg.vocab, 128);
+    if (d_.L < 1 || d_.h % 64 || d_.nh < 1 || d_.h % d_.nh || d_.hd % 64 || d_.s % 128 || d_.B < 1 || d_.V < 2 ||
+        d_.T() > 16384)
+        throw std::invalid_argument(
+            "trainer: need h % 64 == 0, head_dim % 64 == 0, seq_len % 128 == 0, batch*seq <= 16384");
+    adam_ = cfg.adam;
+    seed_ = cfg.seed ? cfg.seed : 1234;
+    cpu_threads_ = cfg.cpu_threads;
+    ps_ = cfg.priority_sched != 0;
+    int lo = 0, hi = 0;
+    check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
+    check(cudaStreamCreateWithPriority(&s_compute_, cudaStreamNonBlocking, hi), "stream");
+    check(cudaStreamCreateWithPriority(&s_h2d_, cudaStreamNonBlocking, lo), "stream");
+    check(cudaStreamCreateWithPriority(&s_d2h_, cudaStreamNonBlocking, lo), "stream");
+    plan(cfg);
+    allocate_and_init();
+    for (int l = 0; l < 4; ++l) lanes_[l] = std::thread([this, l] { lane_main(l); });
+}
+
+Trainer::~Trainer() {
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : lanes_)
+        if (t.joinable()) t.join();
+    cudaDeviceSynchronize();
+    for (Iter* it : iters_) {
+        for (auto& kv : it->ops) {
+            RtOp& o = kv.second;
+            for (cudaEvent_t e : {o.done_ev, o.start_ev, o.t0, o.t1})
+                if (e) cudaEventDestroy(e);
+        }
+        delete it;
+    }
+    for (size_t i = 1; i < blocks_.size(); ++i) {
+        BlockState& b = blocks_[i];
+        if (b.o) {
+            cudaFreeHost(b.master);
+            cudaFreeHost(b.m1);
+            cudaFreeHost(b.m2);
+            cudaFreeHost(b.host_bf16);
+        } else {
+            cudaFree(b.master);
+            cudaFree(b.m1);
+            cudaFree(b.m2);
+        }
+        if (b.wbuf) cudaFree(b.wbuf);
+        if (b.acts) cudaFree(b.acts);
+    }
+    for (uint16_t* x : x_) cudaFree(x);
+    for (void* p : {(void*)gx_[0], (void*)gx_[1], ws_mem_, (void*)wte_, (void*)wte_m_, (void*)wte_v_, (void*)wpe_,
+                    (void*)wpe_m_, (void*)wpe_v_, (void*)lnf_, (void*)lnf_m_, (void*)lnf_v_, (void*)wte_b_,
+                    (void*)wpe_b_, (void*)lnf_b_, (void*)dwte_, (void*)dwpe_, (void*)dwte_b_, (void*)dwpe_b_,
+                    (void*)dlnf_b_, (void*)logits_, (void*)xf_, (void*)meanf_, (void*)rstdf_, (void*)losses_,
+                    (void*)loss_dev_, (void*)tok_dev_})
+        if (p) cudaFree(p);
+    if (loss_host_) cudaFreeHost(loss_host_);
+    if (tok_host_) cudaFreeHost(tok_host_);
+    cudaStreamDestroy(s_compute_);
+    cudaStreamDestroy(s_h2d_);
+    cudaStreamDestroy(s_d2h_);
+}
+
+// ---------------------------------------------------------------------------------------
+// Planning: profile from the real block shape, then the reference planner API.
+// ---------------------------------------------------------------------------------------
+void Trainer::plan(const ah_trainer_config& cfg) {
+    const size_t T = d_.T(), h = d_.h;
+    hetsim::ModelSpec spec;
+    spec.num_blocks = d_.L;
+    spec.hidden_size = d_.h;
+    spec.seq_len = d_.s;
+    spec.batch_size = d_.B;
+    spec.vocab_size = d_.V;
+    // Real activation bytes of a block (input + saved set) over the 2*b*s*h unit.
+    spec.activation_coef = (double)(BlockActs::bytes(d_) + T * h * 2) / (double)(2 * T * h);
+    spec.bwd_fwd_ratio = 2.0;
+    hw_.gpu_mem = cfg.gpu_mem_budget;
+    hw_.cpu_mem = cfg.cpu_mem_budget;
+    hw_.gpu_compute_rate = cfg.gpu_flops;
+    hw_.h2d_bandwidth = cfg.h2d_bw;
+    hw_.d2h_bandwidth = cfg.d2h_bw;
+    hw_.cpu_optim_rate = cfg.cpu_adam_rate;
+    hw_.gpu_optim_rate = cfg.gpu_adam_rate;
+    // Constant GPU residue of this runtime: embedding/positions/final-LN state (fp32 master,
+    // m, v, bf16 copy, fp32 + bf16 grads), logits, head scratch, residual streams, workspace.
+    const size_t emb = (size_t)d_.Vp * h + (size_t)d_.s * h + 2 * h;
+    size_t m_gc = emb * (12 + 2 + 4 + 2) + T * (size_t)d_.Vp * 2 + T * h * 2 + T * 16;
+    m_gc += (size_t)(d_.L + 1) * T * h * 2 + 2 * T * h * 2 + Workspace::bytes(d_);
+    hetsim::ProfileOverrides ov;
+    ov.m_gc = (std::int64_t)m_gc;
+    profile_ = hetsim::build_profile(spec, hw_, ov);
+    const int L = d_.L;
+    if (cfg.c_hat >= 0 && cfg.p_hat >= 0 && cfg.o_hat >= 0) {
+        strategy_ = hetsim::Strategy::uniform(cfg.c_hat, cfg.p_hat, cfg.o_hat, L);
+        if (cfg.prefetch_lookahead)
+            for (int i = 0; i < L; ++i) strategy_.prefetch_lookahead[(size_t)i] = cfg.prefetch_lookahead[i];
+        strategy_.validate(L);
+    } else {
+        hetsim::PlanRequest req;
+        req.profile = profile_;
+        req.hardware = hw_;
+        strategy_ = hetsim::solve(req).strategy;
+    }
+    if (cfg.fine_tune) strategy_ = hetsim::fine_tune_prefetch(profile_, strategy_, hw_);
+    sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    for (const hetsim::CompletedOp& op : sim_.trace) {
+        if (op.iter > 2) continue;
+        order_[op.iter - 1][lane_of(op.kind)].push_back({(int)op.kind, op.block, op.backward_copy});
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+void Trainer::allocate_and_init() {
+    const size_t T = d_.T(), h = d_.h, mp = d_.m_p();
+    const BlockLayout lay = BlockLayout::make(h);
+    check(cudaDeviceGetDefaultMemPool(&pool_, 0), "mempool");
+    uint64_t thr = UINT64_MAX;
+    check(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+    size_t stat = 0;
+    auto dalloc = [&](void** p, size_t bytes) {
+        check(cudaMalloc(p, bytes), "cudaMalloc");
+        stat += bytes;
+    };
+    x_.assign((size_t)d_.L + 1, nullptr);
+    for (auto& x : x_) dalloc((void**)&x, T * h * 2);
+    dalloc((void**)&gx_[0], T * h * 2);
+    dalloc((void**)&gx_[1], T * h * 2);
+    dalloc(&ws_mem_, Workspace::bytes(d_));
+    ws_ = Workspace::carve(d_, ws_mem_);
+    const size_t nwte = (size_t)d_.Vp * h, nwpe = (size_t)d_.s * h;
+    for (float** p : {&wte_, &wte_m_, &wte_v_, &dwte_}) dalloc((void**)p, nwte * 4);
+    for (float** p : {&wpe_, &wpe_m_, &wpe_v_, &dwpe_}) dalloc((void**)p, nwpe * 4);
+    for (float** p : {&lnf_, &lnf_m_, &lnf_v_}) dalloc((void**)p, 2 * h * 4);
+    dalloc((void**)&wte_b_, nwte * 2);
+    dalloc((void**)&dwte_b_, nwte * 2);
+    dalloc((void**)&wpe_b_, nwpe * 2);
+    dalloc((void**)&dwpe_b_, nwpe * 2);
+    dalloc((void**)&lnf_b_, 2 * h * 2);
+    dalloc((void**)&dlnf_b_, 2 * h * 2);
+    dalloc((void**)&logits_, T * (size_t)d_.Vp * 2);
+    dalloc((void**)&xf_, T * h * 2);
+    for (float** p : {&meanf_, &rstdf_, &losses_}) dalloc((void**)p, T * 4);
+    dalloc((void**)&loss_dev_, 256);
+    inv_words_ = 5 * T + 8;
+    dalloc((void**)&tok_dev_, 2 * inv_words_ * 4);
+    check(cudaHostAlloc((void**)&loss_host_, 64, cudaHostAllocPortable), "host alloc");
+    check(cudaHostAlloc((void**)&tok_host_, 2 * 2 * T * 4, cudaHostAllocPortable), "host alloc");
+
+    cudaStream_t st = s_compute_;
+    const float std_res = 0.02f / std::sqrt(2.f * d_.L);
+    float* tmp = nullptr;
+    uint16_t* tmpb = nullptr;
+    check(cudaMalloc(&tmp, mp * 4), "tmp");
+    check(cudaMalloc(&tmpb, mp * 2), "tmp");
+    blocks_.assign((size_t)d_.L + 1, BlockState{});
+    const int L = d_.L;
+    for (int i = 1; i <= L; ++i) {
+        BlockState& b = blocks_[(size_t)i];
+        b.c = i <= strategy_.c_hat;
+        b.p = i <= strategy_.p_hat;
+        b.o = i > L - strategy_.o_hat;
+        const unsigned long long s = seed_ * 1000003ull + (unsigned long long)i * 7919ull;
+        check(gpt::init_normal(tmp + lay.w_qkv, 3 * h * h, s + 1, 0.f, 0.02f, st), "init");
+        check(gpt::init_normal(tmp + lay.w_proj, h * h, s + 2, 0.f, std_res, st), "init");
+        check(gpt::init_normal(tmp + lay.w_fc, 4 * h * h, s + 3, 0.f, 0.02f, st), "init");
+        check(gpt::init_normal(tmp + lay.w_fc2, 4 * h * h, s + 4, 0.f, std_res, st), "init");
+        check(gpt::fill_f32(tmp + lay.b_qkv, lay.ln1_g - lay.b_qkv, 0.f, st), "init");
+        check(gpt::fill_f32(tmp + lay.ln1_g, h, 1.f, st), "init");
+        check(gpt::fill_f32(tmp + lay.ln1_b, h, 0.f, st), "init");
+        check(gpt::fill_f32(tmp + lay.ln2_g, h, 1.f, st), "init");
+        check(gpt::fill_f32(tmp + lay.ln2_b, h, 0.f, st), "init");
+        if (b.o) {
+            // optimizer state in pinned host DRAM: 12 B/param + shared 2 B param/grad buffer
+            check(cudaHostAlloc((void**)&b.master, mp * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.m1, mp * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.m2, mp * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.host_bf16, mp * 2, cudaHostAllocPortable), "host alloc");
+            check(launch_cast_f32_bf16(tmp, tmpb, mp, st), "cast");
+            check(cudaMemcpyAsync(b.master, tmp, mp * 4, cudaMemcpyDeviceToHost, st), "copy");
+            check(cudaMemcpyAsync(b.host_bf16, tmpb, mp * 2, cudaMemcpyDeviceToHost, st), "copy");
+            check(cudaStreamSynchronize(st), "sync");
+            std::memset(b.m1, 0, mp * 4);
+            std::memset(b.m2, 0, mp * 4);
+        } else {
+            dalloc((void**)&b.master, mp * 4);
+            dalloc((void**)&b.m1, mp * 4);
+            dalloc((void**)&b.m2, mp * 4);
+            check(cudaMemcpyAsync(b.master, tmp, mp * 4, cudaMemcpyDeviceToDevice, st), "copy");
+            check(cudaMemsetAsync(b.m1, 0, mp * 4, st), "memset");
+            check(cudaMemsetAsync(b.m2, 0, mp * 4, st), "memset");
+        }
+    }
+    check(cudaStreamSynchronize(st), "sync");
+    cudaFree(tmp);
+    cudaFree(tmpb);
+    // embedding / positions / final LN
+    check(gpt::init_normal(wte_, (size_t)d_.V * h, seed_ * 31 + 5, 0.f, 0.02f, st), "init");
+    check(gpt::fill_f32(wte_ + (size_t)d_.V * h, (size_t)(d_.Vp - d_.V) * h, 0.f, st), "init");
+    check(gpt::init_normal(wpe_, nwpe, seed_ * 31 + 6, 0.f, 0.01f, st), "init");
+    check(gpt::fill_f32(lnf_, h, 1.f, st), "init");
+    check(gpt::fill_f32(lnf_ + h, h, 0.f, st), "init");
+    for (float* p : {wte_m_, wte_v_}) check(cudaMemsetAsync(p, 0, nwte * 4, st), "memset");
+    for (float* p : {wpe_m_, wpe_v_}) check(cudaMemsetAsync(p, 0, nwpe * 4, st), "memset");
+    for (float* p : {lnf_m_, lnf_v_}) check(cudaMemsetAsync(p, 0, 2 * h * 4, st), "memset");
+    check(launch_cast_f32_bf16(wte_, wte_b_, nwte, st), "cast");
+    check(launch_cast_f32_bf16(wpe_, wpe_b_, nwpe, st), "cast");
+    check(launch_cast_f32_bf16(lnf_, lnf_b_, 2 * h, st), "cast");
+    check(cudaStreamSynchronize(st), "sync");
+    static_bytes_ = stat;
+}
+
+// ---------------------------------------------------------------------------------------
+// Iteration construction: the reference op DAG + executor-only physical dependencies.
+// ---------------------------------------------------------------------------------------
+void Trainer::build_iteration(Iter& it) {
+    const int ksim = it.k <= 1 ? 1 : 2;
+    const std::vector<hetsim::StreamOp> ops = hetsim::build_iteration_ops(profile_, strategy_, ksim);
+    for (const hetsim::StreamOp& so : ops) {
+        RtOp r;
+        r.kind = so.kind;
+        r.block = so.block;
+        r.bwd = so.backward_copy;
+        r.iter = it.k;
+        r.lane = lane_of(so.kind);
+        for (const hetsim::OpRef& d : so.deps)
+            r.deps.push_back({it.k - (ksim - d.iter), OpKey{(int)d.kind, d.block, d.backward_copy}});
+        for (const hetsim::OpRef& g : so.start_after_start_of)
+            r.gates.push_back({it.k, OpKey{(int)g.kind, g.block, g.backward_copy}});
+        // Physical requirement not in the timing model: a recompute needs the block's bf16
+        // weights, which for P-blocks arrive with the backward prefetch.
+        if (so.kind == OpKind::Recompute && so.block <= strategy_.p_hat)
+            r.deps.push_back({it.k, OpKey{(int)OpKind::ParamPrefetch, so.block, true}});
+        check(cudaEventCreateWithFlags(&r.done_ev, cudaEventDisableTiming), "event");
+        check(cudaEventCreateWithFlags(&r.start_ev, cudaEventDisableTiming), "event");
+        if (r.lane != kCpu) {
+            check(cudaEventCreate(&r.t0), "event");
+            check(cudaEventCreate(&r.t1), "event");
+        }
+        it.ops.emplace(OpKey{(int)so.kind, so.block, so.backward_copy}, std::move(r));
+    }
+    for (int l = 0; l < 4; ++l) it.lane_order[l] = order_[ksim - 1][l];
+}
+
+Trainer::RtOp* Trainer::find(long long iter, const OpKey& key) {
+    for (Iter* it : iters_)
+        if (it->k == iter) {
+            auto f = it->ops.find(key);
+            return f == it->ops.end() ? nullptr : &f->second;
+        }
+    return nullptr;
+}
+
+void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate) {
+    if (iter < 1) return;
+    cudaEvent_t ev = nullptr;
+    int dep_lane = 0;
+    {
+        std::unique_lock<std::mutex> lk(mu_);
+        RtOp* d = find(iter, key);
+        if (!d) return;  // retired => long complete
+        dep_lane = d->lane;
+        const int need = gate ? 1 : (d->lane == kCpu ? 3 : 2);
+        cv_.wait(lk, [&] { return d->state >= need || stop_; });
+        if (stop_) return;
+        if (d->lane == kCpu) return;  // host ordering already established
+        ev = gate ? d->start_ev : d->done_ev;
+    }
+    if (dep_lane == lane && !gate) return;  // same in-order stream
+    if (lane == kCpu)
+        check(cudaEventSynchronize(ev), "event sync");
+    else
+        check(cudaStreamWaitEvent(stream_of(lane), ev, 0), "stream wait");
+}
+
+void Trainer::lane_main(int lane) {
+    try {
+        long long next = 1;
+        while (true) {
+            Iter* it = nullptr;
+            {
+                std::unique_lock<std::mutex> lk(mu_);
+                cv_.wait(lk, [&] { return stop_ || submitted_ >= next; });
+                if (stop_) return;
+                for (Iter* x : iters_)
+                    if (x->k == next) it = x;
+            }
+            if (!it) throw std::logic_error("executor: iteration window lost");
+            for (const OpKey& key : it->lane_order[lane]) {
+                RtOp& op = it->ops.at(key);
+                for (const auto& dp : op.deps) wait_dep(lane, dp.first, dp.second, false);
+                for (const auto& gt : op.gates) wait_dep(lane, gt.first, gt.second, true);
+                if (lane == kCpu) {
+                    {
+                        std::lock_guard<std::mutex> lk(mu_);
+                        op.state = 1;
+                    }
+                    cv_.notify_all();
+                    run_cpu(*it, op);
+                    {
+                        std::lock_guard<std::mutex> lk(mu_);
+                        op.state = 3;
+                        lane_stats_[lane].busy_ms += op.host_ms;
+                        lane_stats_[lane].ops += 1;
+                    }
+                    cv_.notify_all();
+                    continue;
+                }
+                cudaStream_t st = stream_of(lane);
+                check(cudaEventRecord(op.start_ev, st), "record");
+                check(cudaEventRecord(op.t0, st), "record");
+                {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    op.state = 1;
+                }
+                cv_.notify_all();
+                if (lane == kCompute)
+                    run_compute(*it, op);
+                else if (lane == kH2D)
+                    run_h2d(*it, op);
+                else
+                    run_d2h(*it, op);
+                check(cudaEventRecord(op.t1, st), "record");
+                check(cudaEventRecord(op.done_ev, st), "record");
+                {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    op.state = 2;
+                }
+                cv_.notify_all();
+            }
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                it->finished_lanes += 1;
+                if (it->finished_lanes == 4) completed_ = std::max(completed_, it->k);
+            }
+            cv_.notify_all();
+            ++next;
+        }
+    } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (error_.empty()) error_ = std::string("lane ") + std::to_string(lane) + ": " + e.what();
+        stop_ = true;
+        cv_.notify_all();
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Lane work
+// ---------------------------------------------------------------------------------------
+void Trainer::upload_inputs(Iter& it) {
+    const size_t T = d_.T();
+    const int slot = (int)(it.k & 1);
+    int32_t* dtok = tok_dev_ + slot * inv_words_;
+    int32_t* dtgt = dtok + T;
+    if (it.on_device) {
+        check(cudaMemcpyAsync(dtok, it.tokens, T * 4, cudaMemcpyDeviceToDevice, s_compute_), "tokens");
+        check(cudaMemcpyAsync(dtgt, it.targets, T * 4, cudaMemcpyDeviceToDevice, s_compute_), "targets");
+    } else {
+        check(cudaMemcpyAsync(dtok, it.tokens, T * 4, cudaMemcpyHostToDevice, s_compute_), "tokens");
+        check(cudaMemcpyAsync(dtgt, it.targets, T * 4, cudaMemcpyHostToDevice, s_compute_), "targets");
+    }
+    int32_t* uniq = dtgt + T;
+    int32_t* offs = uniq + T;
+    int32_t* pos = offs + T + 1;
+    int32_t* nuniq = pos + T;
+    check(gpt::token_index(dtok, (int)T, uniq, offs, pos, nuniq, s_compute_), "token index");
+}
+
+void Trainer::embed_forward(Iter& it) {
+    upload_inputs(it);
+    const int32_t* dtok = tok_dev_ + (it.k & 1) * inv_words_;
+    check(gpt::embed_fwd(dtok, wte_b_, wpe_b_, x_[0], d_.T(), d_.s, d_.h, s_compute_), "embed");
+}
+
+void Trainer::head_forward_backward(Iter& it) {
+    const int T = d_.T(), h = d_.h;
+    const int32_t* dtgt = tok_dev_ + (it.k & 1) * inv_words_ + T;
+    cudaStream_t st = s_compute_;
+    check(gpt::ln_fwd(x_[(size_t)d_.L], lnf_b_, lnf_b_ + h, xf_, meanf_, rstdf_, T, h, st), "lnf");
+    gemm::GemmArgs g;
+    g.M = T; g.N = d_.Vp; g.K = h;
+    g.A = xf_; g.lda = h; g.B = wte_b_; g.ldb = h; g.C = logits_; g.ldc = d_.Vp;
+    check(gemm::run(g, st), "logits");
+    check(gpt::cross_entropy(logits_, dtgt, losses_, T, d_.V, d_.Vp, 1.f / T, st), "ce");
+    check(gpt::mean_loss(losses_, T, loss_dev_, st), "loss");
+    check(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, st), "loss d2h");
+    gemm::GemmArgs dg;  // dxf = dlogits . wte
+    dg.M = T; dg.N = h; dg.K = d_.Vp;
+    dg.A = logits_; dg.lda = d_.Vp; dg.B = wte_b_; dg.b_mn_major = 1; dg.ldb = h; dg.C = ws_.dln; dg.ldc = h;
+    check(gemm::run(dg, st), "head dgrad");
+    gemm::GemmArgs wg;  // dwte (fp32) = dlogits^T . xf
+    wg.M = d_.Vp; wg.N = h; wg.K = T;
+    wg.A = logits_; wg.a_mn_major = 1; wg.lda = d_.Vp; wg.B = xf_; wg.b_mn_major = 1; wg.ldb = h;
+    wg.C = dwte_; wg.c_f32 = 1; wg.ldc = h;
+    check(gemm::run(wg, st), "head wgrad");
+    check(gpt::ln_bwd(ws_.dln, x_[(size_t)d_.L], meanf_, rstdf_, lnf_b_, nullptr, gx_[d_.L & 1], dlnf_b_, ws_.part,
+                      T, h, st),
+          "lnf bwd");
+}
+
+void Trainer::embed_backward_and_update(Iter& it) {
+    const int T = d_.T(), h = d_.h;
+    cudaStream_t st = s_compute_;
+    int32_t* base = tok_dev_ + (it.k & 1) * inv_words_;
+    int32_t* uniq = base + 2 * T;
+    int32_t* offs = uniq + T;
+    int32_t* pos = offs + T + 1;
+    int32_t* nuniq = pos + T;
+    const uint16_t* dx0 = gx_[0];
+    check(gpt::embed_bwd_tok_dev(dx0, uniq, offs, pos, nuniq, T, dwte_, h, st), "embed bwd");
+    check(gpt::embed_bwd_pos(dx0, dwpe_, d_.B, d_.s, h, st), "pos bwd");
+    const size_t nwte = (size_t)d_.Vp * h, nwpe = (size_t)d_.s * h;
+    check(gpt::f32_to_bf16(dwte_, dwte_b_, nwte, st), "cvt");
+    check(gpt::f32_to_bf16(dwpe_, dwpe_b_, nwpe, st), "cvt");
+    const int step = (int)it.k;
+    check(launch_adam(adam_args(adam_, step, wte_, wte_m_, wte_v_, dwte_b_, wte_b_, nwte), st), "adam wte");
+    check(launch_adam(adam_args(adam_, step, wpe_, wpe_m_, wpe_v_, dwpe_b_, wpe_b_, nwpe), st), "adam wpe");
+    check(launch_adam(adam_args(adam_, step, lnf_, lnf_m_, lnf_v_, dlnf_b_, lnf_b_, 2 * (size_t)h), st), "adam lnf");
+}
+
+void Trainer::run_compute(Iter& it, RtOp& op) {
+    const int i = op.block;
+    BlockState& b = blocks_[(size_t)i];
+    cudaStream_t st = s_compute_;
+    const size_t mp = d_.m_p();
+    auto materialize = [&]() {  // bf16 weights from the on-GPU fp32 master (footnote 2)
+        check(cudaMallocAsync((void**)&b.wbuf, mp * 2, st), "alloc wbuf");
+        check(launch_cast_f32_bf16(b.master, b.wbuf, mp, st), "cast");
+    };
+    auto alloc_acts = [&]() { check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts"); };
+    auto free_acts = [&]() {
+        check(cudaFreeAsync(b.acts, st), "free acts");
+        b.acts = nullptr;
+    };
+    auto free_wbuf = [&]() {
+        check(cudaFreeAsync(b.wbuf, st), "free wbuf");
+        b.wbuf = nullptr;
+    };
+    switch (op.kind) {
+        case OpKind::Forward: {
+            if (i == 1) embed_forward(it);
+            if (!b.o) materialize();
+            if (!b.wbuf) throw std::logic_error("forward without resident weights");
+            alloc_acts();
+            const BlockActs a = BlockActs::carve(d_, b.acts);
+            check(block_forward(d_, b.wbuf, x_[(size_t)i - 1], x_[(size_t)i], a, ws_, st), "block fwd");
+            if (i == d_.L) head_forward_backward(it);
+            if (b.c) free_acts();
+            if (!b.o || b.p) free_wbuf();
+            break;
+        }
+        case OpKind::Recompute: {
+            if (!b.wbuf) materialize();  // plain C-block: B's materialisation moves up to R
+            alloc_acts();
+            const BlockActs a = BlockActs::carve(d_, b.acts);
+            check(block_forward(d_, b.wbuf, x_[(size_t)i - 1], nullptr, a, ws_, st), "recompute");
+            break;
+        }
+        case OpKind::Backward: {
+            if (!b.wbuf) materialize();
+            const BlockActs a = BlockActs::carve(d_, b.acts);
+            check(block_backward(d_, b.wbuf, x_[(size_t)i - 1], a, gx_[i & 1], gx_[(i - 1) & 1], ws_, st),
+                  "block bwd");
+            free_acts();
+            if (i == 1) embed_backward_and_update(it);
+            break;
+        }
+        case OpKind::GpuOptim: {
+            check(launch_adam(adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf, nullptr, mp), st), "adam");
+            free_wbuf();
+            break;
+        }
+        default:
+            throw std::logic_error("compute lane got a non-compute op");
+    }
+}
+
+void Trainer::run_h2d(Iter& it, RtOp& op) {
+    (void)it;
+    BlockState& b = blocks_[(size_t)op.block];
+    const size_t mp = d_.m_p();
+    check(cudaMallocAsync((void**)&b.wbuf, mp * 2, s_h2d_), "alloc prefetch");
+    if (b.o)
+        check(cudaMemcpyAsync(b.wbuf, b.host_bf16, mp * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
+    else  // P\O backward prefetch: the fp32 master is on the GPU; materialise without PCIe
+        check(launch_cast_f32_bf16(b.master, b.wbuf, mp, s_h2d_), "prefetch cast");
+}
+
+void Trainer::run_d2h(Iter& it, RtOp& op) {
+    (void)it;
+    BlockState& b = blocks_[(size_t)op.block];
+    const size_t mp = d_.m_p();
+    check(cudaMemcpyAsync(b.host_bf16, b.wbuf, mp * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
+    check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
+    b.wbuf = nullptr;
+}
+
+void Trainer::run_cpu(Iter& it, RtOp& op) {
+    BlockState& b = blocks_[(size_t)op.block];
+    ah_adam_hparams hp = adam_;
+    hp.step = (int)it.k;
+    const auto t0 = Clock::now();
+    cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, d_.m_p(), 1.f, cpu_threads_);
+    op.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+// ---------------------------------------------------------------------------------------
+// Public
+// ---------------------------------------------------------------------------------------
+void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_device) {
+    Iter* it = new Iter;
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!error_.empty()) {
+            delete it;
+            throw std::runtime_error(error_);
+        }
+        it->k = submitted_ + 1;
+    }
+    it->on_device = on_device;
+    if (on_device) {
+        it->tokens = tokens;
+        it->targets = targets;
+    } else {  // stage into pinned memory so the H2D copy is truly asynchronous
+        const size_t T = d_.T();
+        int32_t* stage = tok_host_ + (it->k & 1) * 2 * T;
+        // the previous user of this staging slot (iteration k-2) must have consumed it
+        {
+            std::unique_lock<std::mutex> lk(mu_);
+            for (Iter* x : iters_)
+                if (x->k == it->k - 2) {
+                    RtOp* f1 = nullptr;
+                    auto f = x->ops.find(OpKey{(int)OpKind::Forward, 1, false});
+                    if (f != x->ops.end()) f1 = &f->second;
+                    if (f1) {
+                        cv_.wait(lk, [&] { return f1->state >= 2 || stop_; });
+                        cudaEvent_t e = f1->done_ev;
+                        lk.unlock();
+                        check(cudaEventSynchronize(e), "staging reuse");
+                        lk.lock();
+                    }
+                }
+        }
+        std::memcpy(stage, tokens, T * 4);
+        std::memcpy(stage + T, targets, T * 4);
+        it->tokens = stage;
+        it->targets = stage + T;
+    }
+    build_iteration(*it);
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        iters_.push_back(it);
+        submitted_ = it->k;
+        // retire iterations that no live op can reference any more
+        while (iters_.size() > 4 && iters_.front()->k + 3 <= completed_) {
+            Iter* old = iters_.front();
+            retired_.push_back(old);
+            iters_.pop_front();
+        }
+    }
+    cv_.notify_all();
+    for (Iter* old : retired_) {
+        for (auto& kv : old->ops) {
+            RtOp& o = kv.second;
+            if (o.lane != kCpu && o.host_ms >= 0) {  // account GPU lane time before the events go
+                float ms = 0.f;
+                if (cudaEventSynchronize(o.t1) == cudaSuccess && cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
+                    std::lock_guard<std::mutex> lk(mu_);
+                    lane_stats_[o.lane].busy_ms += ms;
+                    lane_stats_[o.lane].ops += 1;
+                }
+            }
+            for (cudaEvent_t e : {o.done_ev, o.start_ev, o.t0, o.t1})
+                if (e) cudaEventDestroy(e);
+        }
+        delete old;
+    }
+    retired_.clear();
+}
+
+float Trainer::drain() {
+    {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || completed_ >= submitted_; });
+        if (!error_.empty()) throw std::runtime_error(error_);
+    }
+    check(cudaStreamSynchronize(s_compute_), "sync");
+    check(cudaStreamSynchronize(s_h2d_), "sync");
+    check(cudaStreamSynchronize(s_d2h_), "sync");
+    // accumulate GPU lane busy time of finished iterations
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (Iter* it : iters_)
+            for (auto& kv : it->ops) {
+                RtOp& o = kv.second;
+                if (o.lane == kCpu || o.host_ms < 0) continue;
+                float ms = 0.f;
+                if (cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
+                    lane_stats_[o.lane].busy_ms += ms;
+                    lane_stats_[o.lane].ops += 1;
+                }
+                o.host_ms = -1.0;  // counted
+            }
+    }
+    last_loss_ = *loss_host_;
+    return last_loss_;
+}
+
+float Trainer::step(const int32_t* tokens, const int32_t* targets) {
+    submit(tokens, targets, false);
+    return drain();
+}
+
+size_t Trainer::master_size(int block) const {
+    if (block >= 1 && block <= d_.L) return d_.m_p();
+    if (block == 0) return (size_t)d_.Vp * d_.h;
+    if (block == -1) return (size_t)d_.s * d_.h;
+    if (block == -2) return 2 * (size_t)d_.h;
+    return 0;
+}
+
+void Trainer::read_master(int block, float* out, size_t n) {
+    const size_t want = master_size(block);
+    if (want == 0 || n < want) throw std::invalid_argument("read_master: bad block or buffer too small");
+    const float* src = nullptr;
+    bool host = false;
+    if (block >= 1) {
+        src = blocks_[(size_t)block].master;
+        host = blocks_[(size_t)block].o;
+    } else {
+        src = block == 0 ? wte_ : (block == -1 ? wpe_ : lnf_);
+    }
+    if (host)
+        std::memcpy(out, src, want * 4);
+    else
+        check(cudaMemcpy(out, src, want * 4, cudaMemcpyDeviceToHost), "read master");
+}
+
+void Trainer::stats(ah_trainer_stats* s) {
+    std::memset(s, 0, sizeof(*s));
+    s->c_hat = strategy_.c_hat;
+    s->p_hat = strategy_.p_hat;
+    s->o_hat = strategy_.o_hat;
+    s->activation_coef = (double)profile_.block.m_a / (double)profile_.block.m_a_in;
+    s->m_p = profile_.block.m_p;
+    s->m_gc = profile_.m_gc;
+    s->modeled_peak_bytes = hetsim::peak_gpu_mem(profile_, strategy_);
+    s->simulated_peak_bytes = sim_.peak_gpu;
+    uint64_t hw = 0;
+    cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hw);
+    s->pool_peak_bytes = (int64_t)hw;
+    s->static_bytes = (int64_t)static_bytes_;
+    s->sim_steady_s = sim_.steady_state_time;
+    std::lock_guard<std::mutex> lk(mu_);
+    for (int l = 0; l < 4; ++l) {
+        s->lane_busy_ms[l] = lane_stats_[l].busy_ms;
+        s->lane_ops[l] = lane_stats_[l].ops;
+    }
+    s->h2d_bytes = (int64_t)2 * profile_.block.m_p * (strategy_.o_hat + std::max(0, strategy_.p_hat));
+    s->d2h_bytes = (int64_t)2 * profile_.block.m_p * strategy_.o_hat;
+}
+
+std::string Trainer::trace_json() {
+    std::ostringstream out;
+    std::vector<hetsim::CompletedOp> ops;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (iters_.empty()) return "[]\n";
+    // time origin: first op of the oldest iteration still in the window
+    cudaEvent_t origin = nullptr;
+    for (auto& kv : iters_.front()->ops)
+        if (kv.second.lane == kCompute && kv.second.kind == OpKind::Forward && kv.second.block == 1)
+            origin = kv.second.t0;
+    for (Iter* it : iters_)
+        for (auto& kv : it->ops) {
+            RtOp& o = kv.second;
+            if (o.lane == kCpu || !origin) continue;
+            float a = 0, b = 0;
+            if (cudaEventElapsedTime(&a, origin, o.t0) != cudaSuccess) continue;
+            if (cudaEventElapsedTime(&b, origin, o.t1) != cudaSuccess) continue;
+            ops.push_back({o.kind, o.block, (int)o.iter, o.bwd, hetsim::stream_of(o.kind), a / 1e3, b / 1e3});
+        }
+    std::sort(ops.begin(), ops.end(), [](const hetsim::CompletedOp& x, const hetsim::CompletedOp& y) {
+        return x.start < y.start;
+    });
+    hetsim::write_chrome_trace(out, ops);
+    return out.str();
+}
+
+}  // namespace ah

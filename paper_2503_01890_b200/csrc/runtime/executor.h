@@ -1,0 +1,169 @@
+// B200 executor for the AutoHete iteration: realises the hetsim op DAG
+// (build_iteration_ops, reference proj/core/src/simulator.cpp:91-229) on four lanes —
+// a high-priority compute stream, an H2D copy stream, a D2H copy stream and a host CPU
+// worker — in the per-lane order produced by the reference scheduler (priority-based or
+// FIFO, simulator.cpp:413-450). Each lane is driven by its own host thread; cross-lane
+// dependencies become cudaStreamWaitEvent (GPU -> GPU), cudaEventSynchronize (GPU -> CPU)
+// or a host condition variable (CPU -> GPU); start-after-start launch gates become events
+// recorded on the compute stream immediately before the gated op.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <condition_variable>
+#include <cstdint>
+#include <deque>
+#include <map>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "autohete.h"
+#include "gpt_model.h"
+#include "hetsim/planner.hpp"
+#include "hetsim/simulator.hpp"
+
+namespace ah {
+
+struct LaneStats {
+    double busy_ms = 0.0;  // host-observed for the CPU lane; event-timed for GPU lanes
+    int ops = 0;
+};
+
+class Trainer {
+public:
+    explicit Trainer(const ah_trainer_config& cfg);
+    ~Trainer();
+
+    // Enqueue one training iteration. tokens/targets: B*s int32, host (pinned or pageable)
+    // unless on_device. Returns immediately; lanes run asynchronously.
+    void submit(const int32_t* tokens, const int32_t* targets, bool on_device);
+    // Block until every submitted iteration finished; returns the last iteration's loss.
+    float drain();
+    // One synchronous iteration (H2D of inputs, full step, D2H of the loss).
+    float step(const int32_t* tokens, const int32_t* targets);
+
+    const hetsim::Strategy& strategy() const { return strategy_; }
+    const hetsim::ModelProfile& profile() const { return profile_; }
+    const GptDims& dims() const { return d_; }
+    const hetsim::SimResult& simulated() const { return sim_; }
+    void stats(ah_trainer_stats* out);
+    // fp32 master of block b (1-based; 0 = embedding wte, -1 = wpe, -2 = final LN) -> host.
+    void read_master(int block, float* out, size_t n);
+    size_t master_size(int block) const;
+    // Chrome trace of the last drained iterations in the reference schema (simulator.cpp:598).
+    std::string trace_json();
+
+private:
+    enum Lane { kCompute = 0, kH2D = 1, kD2H = 2, kCpu = 3 };
+    struct OpKey {
+        int kind, block;
+        bool bwd;
+        bool operator<(const OpKey& o) const {
+            if (kind != o.kind) return kind < o.kind;
+            if (block != o.block) return block < o.block;
+            return bwd < o.bwd;
+        }
+    };
+    struct RtOp {
+        hetsim::OpKind kind;
+        int block = 0;
+        bool bwd = false;
+        long long iter = 0;  // global iteration number (1-based)
+        int lane = 0;
+        std::vector<std::pair<long long, OpKey>> deps;   // (iteration, op)
+        std::vector<std::pair<long long, OpKey>> gates;  // start-after-start (compute ops)
+        cudaEvent_t done_ev = nullptr, start_ev = nullptr, t0 = nullptr, t1 = nullptr;
+        int state = 0;  // 0 pending, 1 started (start_ev recorded), 2 issued (done_ev recorded), 3 done (host)
+        double host_ms = 0.0;
+    };
+    struct Iter {
+        long long k = 0;
+        std::map<OpKey, RtOp> ops;
+        std::vector<OpKey> lane_order[4];
+        const int32_t* tokens = nullptr;
+        const int32_t* targets = nullptr;
+        bool on_device = false;
+        int finished_lanes = 0;
+    };
+    struct BlockState {
+        bool o = false, p = false, c = false;
+        float* master = nullptr;  // device (non-O) or pinned host (O)
+        float* m1 = nullptr;
+        float* m2 = nullptr;
+        uint16_t* host_bf16 = nullptr;  // O blocks: shared param/grad buffer
+        uint16_t* wbuf = nullptr;       // device bf16 weights / grads while resident
+        void* acts = nullptr;           // device activation set while live
+    };
+
+    void plan(const ah_trainer_config& cfg);
+    void allocate_and_init();
+    void build_iteration(Iter& it);
+    void lane_main(int lane);
+    void wait_dep(int lane, long long iter, const OpKey& key, bool gate);
+    RtOp* find(long long iter, const OpKey& key);
+    void run_compute(Iter& it, RtOp& op);
+    void run_h2d(Iter& it, RtOp& op);
+    void run_d2h(Iter& it, RtOp& op);
+    void run_cpu(Iter& it, RtOp& op);
+    void embed_forward(Iter& it);
+    void head_forward_backward(Iter& it);
+    void embed_backward_and_update(Iter& it);
+    void upload_inputs(Iter& it);
+    void check(cudaError_t e, const char* what);
+    cudaStream_t stream_of(int lane) const;
+
+    GptDims d_;
+    hetsim::ModelProfile profile_;
+    hetsim::HardwareSpec hw_;
+    hetsim::Strategy strategy_;
+    hetsim::SimResult sim_;
+    bool ps_ = true;
+    ah_adam_hparams adam_{};
+    unsigned long long seed_ = 1234;
+    int cpu_threads_ = 0;
+    // per-lane compiled order of iteration 1 and of the steady state (iteration 2)
+    std::vector<OpKey> order_[2][4];
+
+    cudaStream_t s_compute_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
+    std::vector<BlockState> blocks_;  // index 1..L
+    std::vector<uint16_t*> x_;        // residual stream x[0..L] (x[0] = embedding output)
+    uint16_t* gx_[2] = {nullptr, nullptr};  // residual-gradient ping-pong
+    void* ws_mem_ = nullptr;
+    Workspace ws_;
+    // head / embedding (GPU-resident, m_gc)
+    float *wte_ = nullptr, *wte_m_ = nullptr, *wte_v_ = nullptr;
+    float *wpe_ = nullptr, *wpe_m_ = nullptr, *wpe_v_ = nullptr;
+    float *lnf_ = nullptr, *lnf_m_ = nullptr, *lnf_v_ = nullptr;
+    uint16_t *wte_b_ = nullptr, *wpe_b_ = nullptr, *lnf_b_ = nullptr;
+    float *dwte_ = nullptr, *dwpe_ = nullptr;
+    uint16_t *dwte_b_ = nullptr, *dwpe_b_ = nullptr, *dlnf_b_ = nullptr;
+    uint16_t* logits_ = nullptr;
+    uint16_t* xf_ = nullptr;
+    float *meanf_ = nullptr, *rstdf_ = nullptr, *losses_ = nullptr, *loss_dev_ = nullptr;
+    float* loss_host_ = nullptr;  // pinned
+    int32_t* tok_dev_ = nullptr;  // [2][T] tokens, [2][T] targets, inverse index
+    int32_t* tok_host_ = nullptr; // pinned staging for inputs + inverse index
+    size_t inv_words_ = 0;
+    int n_uniq_[2] = {0, 0};
+    cudaMemPool_t pool_ = nullptr;
+    size_t static_bytes_ = 0;
+    int gpu_adam_steps_ = 0;
+
+    // iteration window
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<Iter*> iters_;
+    std::vector<Iter*> retired_;
+    long long submitted_ = 0, completed_ = 0;
+    bool stop_ = false;
+    std::string error_;
+    std::thread lanes_[4];
+    size_t lane_pos_[4] = {0, 0, 0, 0};  // index into iters_ window per lane
+    LaneStats lane_stats_[4];
+    float last_loss_ = 0.f;
+};
+
+}  // namespace ah

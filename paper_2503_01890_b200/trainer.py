@@ -1,0 +1,149 @@
+"""Public training API: a GPT model trained on B200 under an AutoHete plan.
+
+    tr = Trainer(ModelConfig(...), PlanConfig(...))
+    loss = tr.step(tokens, targets)          # synchronous, host int32 arrays
+    tr.submit(tokens, targets); tr.drain()   # asynchronous pipelining across iterations
+
+The plan is decided by the drop-in hetsim planner (include/hetsim/planner.hpp, reference
+proj/core/src/planner.cpp:37-153) unless a strategy is forced, and executed by the C++
+executor (csrc/runtime/executor.cpp) through the C-ABI — no Python on the per-op path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import json
+
+import numpy as np
+
+from . import _native as N
+
+
+@dataclasses.dataclass
+class ModelConfig:
+    num_blocks: int = 24
+    hidden: int = 2048
+    heads: int = 16
+    seq_len: int = 1024
+    batch: int = 8
+    vocab: int = 50257
+
+
+@dataclasses.dataclass
+class PlanConfig:
+    c_hat: int = -1  # any < 0: let the planner decide
+    p_hat: int = -1
+    o_hat: int = -1
+    prefetch_lookahead: list[int] | None = None
+    priority_sched: bool = True
+    fine_tune: bool = True
+    gpu_mem_budget: int = 40 << 30
+    cpu_mem_budget: int = 128 << 30
+    gpu_flops: float = 1.0e15
+    h2d_bw: float = 50e9
+    d2h_bw: float = 50e9
+    cpu_adam_rate: float = 1.0e9
+    gpu_adam_rate: float = 2.0e11
+
+
+@dataclasses.dataclass
+class AdamConfig:
+    lr: float = 1e-4
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.01
+
+
+class Trainer:
+    def __init__(self, model: ModelConfig, plan: PlanConfig | None = None, adam: AdamConfig | None = None,
+                 seed: int = 1234, cpu_threads: int = 0):
+        plan = plan or PlanConfig()
+        adam = adam or AdamConfig()
+        self.model = model
+        cfg = N.TrainerConfig()
+        for f in dataclasses.fields(model):
+            setattr(cfg, f.name, getattr(model, f.name))
+        cfg.c_hat, cfg.p_hat, cfg.o_hat = plan.c_hat, plan.p_hat, plan.o_hat
+        self._la = None
+        if plan.prefetch_lookahead is not None:
+            self._la = (C.c_int32 * model.num_blocks)(*plan.prefetch_lookahead)
+            cfg.prefetch_lookahead = C.cast(self._la, C.POINTER(C.c_int32))
+        cfg.priority_sched = int(plan.priority_sched)
+        cfg.fine_tune = int(plan.fine_tune)
+        cfg.gpu_mem_budget, cfg.cpu_mem_budget = plan.gpu_mem_budget, plan.cpu_mem_budget
+        cfg.gpu_flops, cfg.h2d_bw, cfg.d2h_bw = plan.gpu_flops, plan.h2d_bw, plan.d2h_bw
+        cfg.cpu_adam_rate, cfg.gpu_adam_rate = plan.cpu_adam_rate, plan.gpu_adam_rate
+        cfg.adam = N.AdamHParams(adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, 1)
+        cfg.seed = seed
+        cfg.cpu_threads = cpu_threads
+        self._h = C.c_void_p()
+        N.check(N.lib().ah_trainer_create(C.byref(cfg), C.byref(self._h)), "ah_trainer_create")
+
+    def close(self):
+        if self._h:
+            N.check(N.lib().ah_trainer_destroy(self._h), "ah_trainer_destroy")
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _ptr(x):
+        if hasattr(x, "data_ptr"):
+            return x.data_ptr(), bool(x.is_cuda)
+        x = np.ascontiguousarray(x, dtype=np.int32)
+        return x.ctypes.data, False
+
+    def step(self, tokens, targets) -> float:
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        y = np.ascontiguousarray(targets, dtype=np.int32)
+        loss = C.c_float()
+        N.check(N.lib().ah_trainer_step(self._h, t.ctypes.data, y.ctypes.data, C.byref(loss)), "ah_trainer_step")
+        return loss.value
+
+    def submit(self, tokens, targets) -> None:
+        """tokens/targets: host numpy int32, or CUDA int32 tensors (kept alive by the caller)."""
+        if hasattr(tokens, "data_ptr"):
+            N.check(N.lib().ah_trainer_submit(self._h, tokens.data_ptr(), targets.data_ptr(), int(tokens.is_cuda)),
+                    "ah_trainer_submit")
+        else:
+            t = np.ascontiguousarray(tokens, dtype=np.int32)
+            y = np.ascontiguousarray(targets, dtype=np.int32)
+            N.check(N.lib().ah_trainer_submit(self._h, t.ctypes.data, y.ctypes.data, 0), "ah_trainer_submit")
+
+    def drain(self) -> float:
+        loss = C.c_float()
+        N.check(N.lib().ah_trainer_drain(self._h, C.byref(loss)), "ah_trainer_drain")
+        return loss.value
+
+    def stats(self) -> dict:
+        s = N.TrainerStats()
+        N.check(N.lib().ah_trainer_stats_get(self._h, C.byref(s)), "ah_trainer_stats_get")
+        out = {f: getattr(s, f) for f, _ in s._fields_}
+        out["lane_busy_ms"] = list(s.lane_busy_ms)
+        out["lane_ops"] = list(s.lane_ops)
+        return out
+
+    def schedule(self) -> list[str]:
+        n = N.lib().ah_trainer_schedule(self._h, None, 0)
+        buf = C.create_string_buffer(n)
+        N.lib().ah_trainer_schedule(self._h, buf, n)
+        return buf.value.decode().split()
+
+    def master(self, block: int) -> np.ndarray:
+        n = N.lib().ah_trainer_master_size(self._h, block)
+        out = np.empty(n, dtype=np.float32)
+        N.check(N.lib().ah_trainer_read_master(self._h, block, out.ctypes.data, n), "ah_trainer_read_master")
+        return out
+
+    def trace(self) -> list:
+        n = N.lib().ah_trainer_trace(self._h, None, 0)
+        if n < 0:
+            N.check(n, "ah_trainer_trace")
+        buf = C.create_string_buffer(max(n, 1) + 4096)
+        N.check(min(0, N.lib().ah_trainer_trace(self._h, buf, len(buf))), "ah_trainer_trace")
+        return json.loads(buf.value.decode())

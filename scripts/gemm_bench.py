@@ -1,0 +1,44 @@
+"""tcgen05 GEMM throughput on the GPT-1.3B block shapes (T=8192, h=2048) vs torch/cuBLAS."""
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2503_01890_b200.gemm import gemm  # noqa: E402
+
+T, h = 8192, 2048
+SHAPES = [  # name, M, N, K, a_mn, b_mn
+    ("qkv_fwd", T, 3 * h, h, 0, 0), ("proj_fwd", T, h, h, 0, 0), ("fc_fwd", T, 4 * h, h, 0, 0),
+    ("fc2_fwd", T, h, 4 * h, 0, 0),
+    ("fc2_dgrad", T, 4 * h, h, 0, 1), ("fc_wgrad", 4 * h, h, T, 1, 1), ("qkv_wgrad", 3 * h, h, T, 1, 1),
+]
+
+
+def timeit(fn, iters=20):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / 1e3 / iters
+
+
+for name, M, N, K, a_mn, b_mn in SHAPES:
+    A = torch.randn(K, M, device="cuda").bfloat16() if a_mn else torch.randn(M, K, device="cuda").bfloat16()
+    B = torch.randn(K, N, device="cuda").bfloat16() if b_mn else torch.randn(N, K, device="cuda").bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    res = {}
+    for bn in (128, 256):
+        t = timeit(lambda: gemm(A, B, C, a_mn=bool(a_mn), b_mn=bool(b_mn), block_n=bn))
+        res[f"ours_bn{bn}_tflops"] = round(2 * M * N * K / t / 1e12, 1)
+    At = A.t() if a_mn else A
+    Bt = B if b_mn else B.t()
+    t = timeit(lambda: torch.matmul(At, Bt, out=C))
+    res["cublas_tflops"] = round(2 * M * N * K / t / 1e12, 1)
+    print(json.dumps({"shape": name, "M": M, "N": N, "K": K, **res}), flush=True)

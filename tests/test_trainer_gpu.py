@@ -1,0 +1,109 @@
+"""End-to-end GPU tests of the executor: numerics vs a torch fp32 reference, bit-identical
+training state across recompute / offload plans (CPU Adam == GPU Adam, recompute ==
+forward), and the realised per-lane order == the reference scheduler's order."""
+import numpy as np
+import pytest
+import torch
+
+from tests import gpt_reference as ref
+
+pytestmark = pytest.mark.gpu
+
+MODEL = dict(num_blocks=4, hidden=256, heads=2, seq_len=256, batch=2, vocab=1000)
+
+
+def make(plan=None, adam=None, seed=7):
+    from paper_2503_01890_b200.trainer import AdamConfig, ModelConfig, PlanConfig, Trainer
+    return Trainer(ModelConfig(**MODEL), plan or PlanConfig(c_hat=0, p_hat=0, o_hat=0),
+                   adam or AdamConfig(), seed=seed, cpu_threads=4)
+
+
+def batch(seed=0):
+    rng = np.random.default_rng(seed)
+    toks = rng.integers(0, MODEL["vocab"], size=(MODEL["batch"], MODEL["seq_len"]), dtype=np.int32)
+    tgts = rng.integers(0, MODEL["vocab"], size=(MODEL["batch"], MODEL["seq_len"]), dtype=np.int32)
+    return toks, tgts
+
+
+def test_step_matches_torch_reference(cuda_device, native):
+    from paper_2503_01890_b200.trainer import AdamConfig
+    # eps >> |g|, lr = 1, no decay: one AdamW step moves p by -g/(|g|+eps) ~= -g, so the
+    # parameter delta exposes the gradient the CUDA path computed.
+    eps = 1.0
+    tr = make(adam=AdamConfig(lr=1.0, eps=eps, weight_decay=0.0))
+    L, h = MODEL["num_blocks"], MODEL["hidden"]
+    before = [torch.from_numpy(tr.master(i).copy()) for i in range(1, L + 1)]
+    wte = torch.from_numpy(tr.master(0).copy()).view(-1, h)
+    wpe = torch.from_numpy(tr.master(-1).copy()).view(-1, h)
+    lnf = torch.from_numpy(tr.master(-2).copy())
+    toks, tgts = batch()
+    loss = tr.step(toks, tgts)
+    rl, g_blocks, g_wte, g_wpe, g_lnf = ref.loss_and_grads(before, wte, wpe, lnf, torch.from_numpy(toks).long(),
+                                                           torch.from_numpy(tgts).long(), MODEL["heads"],
+                                                           MODEL["vocab"])
+    assert abs(loss - rl) / rl < 1e-2, (loss, rl)
+    for i in range(L):
+        after = torch.from_numpy(tr.master(i + 1).copy())
+        g = g_blocks[i].reshape(-1)
+        est = -(after - before[i])  # = g / (|g| + eps) elementwise
+        exp = g / (g.abs() + eps)
+        err = (est - exp).norm() / exp.norm()
+        assert err < 5e-2, (i, float(err))
+    est = -(torch.from_numpy(tr.master(0).copy()).view(-1, h) - wte)
+    exp = g_wte / (g_wte.abs() + eps)
+    assert (est - exp).norm() / exp.norm() < 5e-2
+    tr.close()
+
+
+PLANS = [
+    dict(c_hat=0, p_hat=0, o_hat=0),
+    dict(c_hat=4, p_hat=0, o_hat=0),
+    dict(c_hat=2, p_hat=0, o_hat=3),
+    dict(c_hat=1, p_hat=2, o_hat=2, prefetch_lookahead=[2, 1, 1, 1]),  # P\O block 1
+    dict(c_hat=3, p_hat=4, o_hat=4, prefetch_lookahead=[1, 2, 1, 1]),  # full offload
+]
+
+
+def run_plan(plan_kw, ps=True, steps=3):
+    from paper_2503_01890_b200.trainer import PlanConfig
+    tr = make(plan=PlanConfig(priority_sched=ps, fine_tune=False, gpu_mem_budget=1 << 40, **plan_kw))
+    losses = []
+    for k in range(steps):
+        toks, tgts = batch(k)
+        tr.submit(toks, tgts)
+    losses.append(tr.drain())
+    state = [tr.master(i).copy() for i in range(-2, MODEL["num_blocks"] + 1)]
+    st = tr.stats()
+    tr.close()
+    return losses, state, st
+
+
+def test_plans_give_bit_identical_training_state(cuda_device, native):
+    base_loss, base_state, _ = run_plan(PLANS[0])
+    for plan in PLANS[1:]:
+        for ps in (True, False):
+            loss, state, st = run_plan(plan, ps=ps)
+            assert (st["c_hat"], st["p_hat"], st["o_hat"]) == (plan["c_hat"], plan["p_hat"], plan["o_hat"])
+            assert loss == base_loss, (plan, ps)
+            for a, b in zip(state, base_state):
+                assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (plan, ps)
+
+
+def test_realised_lane_order_matches_scheduler(cuda_device, native):
+    from paper_2503_01890_b200.trainer import PlanConfig
+    tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=4, priority_sched=True, fine_tune=False,
+                              gpu_mem_budget=1 << 40))
+    toks, tgts = batch()
+    for _ in range(3):
+        tr.submit(toks, tgts)
+    tr.drain()
+    sched = tr.schedule()  # steady-state per-lane order from hetsim::run
+    trace = tr.trace()
+    for lane in ("COMPUTE", "H2D", "D2H"):
+        want = [t.split(":")[1].rstrip("b") for t in sched if t.startswith(lane + ":")]
+        got = [e["name"] for e in trace if e["cat"] == lane]
+        # every realised iteration (window) repeats the simulated lane order
+        n = len(want)
+        assert n > 0
+        assert got[-n:] == want, (lane, got[-n:], want)
+    tr.close()
