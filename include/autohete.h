@@ -149,6 +149,7 @@ typedef struct ah_trainer_config {
     int32_t fine_tune;                 /* run fine_tune_prefetch after solve */
     int64_t gpu_mem_budget, cpu_mem_budget; /* planner budgets, bytes */
     double gpu_flops, h2d_bw, d2h_bw, cpu_adam_rate, gpu_adam_rate; /* HardwareSpec rates */
+    double bwd_fwd_ratio; /* ModelSpec::bwd_fwd_ratio (<= 0 => 2.0) */
     ah_adam_hparams adam;
     uint64_t seed;
     int32_t cpu_threads; /* CPU Adam threads, <= 0 = all */
@@ -186,6 +187,29 @@ int ah_trainer_schedule(void* trainer, char* buf, size_t cap);
 int ah_trainer_read_master(void* trainer, int32_t block, float* out, size_t n);
 int64_t ah_trainer_master_size(void* trainer, int32_t block);
 int ah_trainer_trace(void* trainer, char* buf, size_t cap); /* Chrome trace JSON, measured */
+/* Device-timed region on the executor's compute stream: stop=0 drains then records the
+ * start event; stop=1 drains all lanes, records the stop event and returns elapsed ms. */
+int ah_trainer_timer(void* trainer, int32_t stop, float* ms);
+
+/* ---------------------------------------------------------------------------------------
+ * Runtime profiler (paper §3.1): measures one block on this box and
+ * returns the HardwareSpec rates the planner consumes. Reference counterpart: the analytic
+ * estimate_block_times (proj/core/src/workload.cpp:55-73), which this replaces.
+ * --------------------------------------------------------------------------------------- */
+typedef struct ah_hw_profile {
+    double t_fwd_s, t_bwd_s;  /* one block, measured */
+    double gpu_flops;         /* (2*m_p*b*s + 4*b*s^2*h) / t_fwd_s, workload.cpp:63 */
+    double bwd_fwd_ratio;     /* t_bwd_s / t_fwd_s -> ModelSpec::bwd_fwd_ratio */
+    double h2d_bw, d2h_bw;    /* pinned 2*m_p-byte copies, B/s */
+    double gpu_adam_rate;     /* params/s, fused sm_100a AdamW */
+    double cpu_adam_rate;     /* params/s, host AdamW with cfg->cpu_threads */
+} ah_hw_profile;
+int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out);
+
+/* Instrumentation for the bench: kernels launched by this library so far, and live GEMM
+ * timing (enable=1 starts recording; enable=0 stops and returns totals since enabling). */
+int64_t ah_kernel_launches(void);
+int ah_gemm_timing(int32_t enable, double* total_ms, double* total_flops, int64_t* launches);
 
 #ifdef __cplusplus
 }

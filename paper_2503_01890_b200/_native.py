@@ -127,7 +127,7 @@ class TrainerConfig(C.Structure):
         ("priority_sched", C.c_int32), ("fine_tune", C.c_int32),
         ("gpu_mem_budget", C.c_int64), ("cpu_mem_budget", C.c_int64),
         ("gpu_flops", C.c_double), ("h2d_bw", C.c_double), ("d2h_bw", C.c_double),
-        ("cpu_adam_rate", C.c_double), ("gpu_adam_rate", C.c_double),
+        ("cpu_adam_rate", C.c_double), ("gpu_adam_rate", C.c_double), ("bwd_fwd_ratio", C.c_double),
         ("adam", AdamHParams), ("seed", C.c_uint64), ("cpu_threads", C.c_int32),
     ]
 
@@ -155,4 +155,18 @@ _EXTRA_SIGS.update({
     "ah_trainer_read_master": ([C.c_void_p, C.c_int32, C.c_void_p, C.c_size_t], C.c_int),
     "ah_trainer_master_size": ([C.c_void_p, C.c_int32], C.c_int64),
     "ah_trainer_trace": ([C.c_void_p, C.c_char_p, C.c_size_t], C.c_int),
+})
+
+
+class HwProfile(C.Structure):
+    _fields_ = [("t_fwd_s", C.c_double), ("t_bwd_s", C.c_double), ("gpu_flops", C.c_double),
+                ("bwd_fwd_ratio", C.c_double), ("h2d_bw", C.c_double), ("d2h_bw", C.c_double),
+                ("gpu_adam_rate", C.c_double), ("cpu_adam_rate", C.c_double)]
+
+
+_EXTRA_SIGS.update({
+    "ah_trainer_timer": ([C.c_void_p, C.c_int32, C.POINTER(C.c_float)], C.c_int),
+    "ah_profile_block": ([C.POINTER(TrainerConfig), C.POINTER(HwProfile)], C.c_int),
+    "ah_kernel_launches": ([], C.c_int64),
+    "ah_gemm_timing": ([C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
 })

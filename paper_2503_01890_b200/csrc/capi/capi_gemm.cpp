@@ -21,3 +21,20 @@ extern "C" int ah_gemm_bf16(const ah_gemm_desc* d, void* stream) {
     if ((g.epilogue & AH_EPI_AUX) && !g.aux) return ah::set_error(AH_ERR_INVALID, "ah_gemm_bf16: aux missing");
     return ah::cuda_status(ah::gemm::run(g, static_cast<cudaStream_t>(stream)), "ah_gemm_bf16");
 }
+
+#include "../kernels/kernels.h"
+
+extern "C" int64_t ah_kernel_launches(void) { return ah::kernel_launch_counter().load(); }
+
+extern "C" int ah_gemm_timing(int32_t enable, double* total_ms, double* total_flops, int64_t* launches) {
+    if (enable) {
+        ah::gemm::timing_collect(nullptr, nullptr, nullptr);  // drop stale records
+        ah::gemm::timing_enable(true);
+        return AH_OK;
+    }
+    ah::gemm::timing_enable(false);
+    long long n = 0;
+    ah::gemm::timing_collect(total_ms, total_flops, &n);
+    if (launches) *launches = n;
+    return AH_OK;
+}

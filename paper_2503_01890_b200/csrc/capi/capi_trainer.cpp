@@ -115,3 +115,24 @@ int ah_trainer_trace(void* tr, char* buf, size_t cap) {
 }
 
 }  // extern "C"
+
+namespace ah {
+ah_hw_profile profile_block(const ah_trainer_config& cfg);
+}
+
+extern "C" {
+
+int ah_trainer_timer(void* tr, int32_t stop, float* ms) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    return guarded([&] {
+        const float v = T(tr)->timer(stop != 0);
+        if (ms) *ms = v;
+    });
+}
+
+int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out) {
+    if (!cfg || !out) return ah::set_error(AH_ERR_INVALID, "ah_profile_block: null argument");
+    return guarded([&] { *out = ah::profile_block(*cfg); });
+}
+
+}  // extern "C"

@@ -251,7 +251,7 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
         adam_scalar_kernel<<<grid, 256, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, done, a.n, k,
                                                       a.skip, a.stats);
     }
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t launch_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t stream) {
@@ -263,7 +263,7 @@ cudaError_t launch_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, cuda
         done = n_vec * 8;
     }
     if (done < n) cast_tail_kernel<<<1, 256, 0, stream>>>(src, dst, done, n);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, float* stats,
@@ -272,7 +272,7 @@ cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, floa
     const bool vec = aligned16(g);
     grad_stats_kernel<<<grid_for(vec ? n / 8 + 1 : n, 256, 8), 256, 0, stream>>>(g, n, inv_scale,
                                                                                stats, vec);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 }  // namespace ah

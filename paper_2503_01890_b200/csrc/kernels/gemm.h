@@ -52,3 +52,14 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas = 0);
 
 }  // namespace gemm
 }  // namespace ah
+
+namespace ah {
+namespace gemm {
+// Live per-launch timing of the GEMM (bench roofline): when enabled, every launch is
+// bracketed by CUDA events on its stream; collect() sums durations and executed FLOPs.
+void timing_enable(bool on);
+void timing_collect(double* total_ms, double* total_flops, long long* launches);
+// FLOPs a launch actually executes (causal tile / K-range skipping included).
+double executed_flops(const GemmArgs& g);
+}  // namespace gemm
+}  // namespace ah

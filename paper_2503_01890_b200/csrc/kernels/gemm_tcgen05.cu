@@ -25,10 +25,13 @@
 #include <cuda.h>
 
 #include <cstdio>
+#include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm.h"
+#include "kernels.h"
 
 namespace ah {
 namespace gemm {
@@ -453,7 +456,67 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const 
         configured = true;
     }
     gemm_kernel<BN, STAGES><<<grid, kThreads, sm, stream>>>(a, b, P);
-    return cudaGetLastError();
+    return launched(1);
+}
+
+struct TimingState {
+    std::mutex mu;
+    bool on = false;
+    struct Rec {
+        cudaEvent_t a, b;
+        double flops;
+    };
+    std::vector<Rec> recs;
+};
+static TimingState& timing() {
+    static TimingState t;
+    return t;
+}
+
+void timing_enable(bool on) {
+    std::lock_guard<std::mutex> lk(timing().mu);
+    timing().on = on;
+}
+
+void timing_collect(double* total_ms, double* total_flops, long long* launches) {
+    std::lock_guard<std::mutex> lk(timing().mu);
+    double ms = 0.0, fl = 0.0;
+    long long n = 0;
+    for (auto& r : timing().recs) {
+        float t = 0.f;
+        cudaEventSynchronize(r.b);
+        if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+            ms += t;
+            fl += r.flops;
+            ++n;
+        }
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    timing().recs.clear();
+    if (total_ms) *total_ms = ms;
+    if (total_flops) *total_flops = fl;
+    if (launches) *launches = n;
+}
+
+double executed_flops(const GemmArgs& g) {
+    int BN = g.block_n;
+    if (BN == 0) BN = g.N >= 256 ? 256 : (g.N > 64 ? 128 : 64);
+    const long long tiles_m = (g.M + BM - 1) / BM, tiles_n = (g.N + BN - 1) / BN, kb = (g.K + BK - 1) / BK;
+    double f = 0.0;
+    for (long long tm = 0; tm < tiles_m; ++tm) {
+        const long long m0 = tm * BM, mrows = std::min<long long>(BM, g.M - m0);
+        long long k0 = 0, k1 = kb;
+        if (g.causal == kCausalKUptoM) k1 = std::min<long long>(kb, (m0 + BM + BK - 1) / BK);
+        if (g.causal == kCausalKFromM) k0 = m0 / BK;
+        if (k0 >= k1) continue;
+        const long long kl = std::min<long long>(g.K, k1 * BK) - k0 * BK;
+        for (long long tn = 0; tn < tiles_n; ++tn) {
+            if (g.causal == kCausalSkipUpper && tn * BN > m0 + BM - 1) continue;
+            f += 2.0 * mrows * std::min<long long>(BN, g.N - tn * BN) * kl;
+        }
+    }
+    return f * std::max(1, g.batch1) * std::max(1, g.batch2);
 }
 
 cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
@@ -511,9 +574,30 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
     int grid = P.num_tiles < kNumSMs ? P.num_tiles : kNumSMs;
     if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
-    if (BN == 256) return launch_cfg<256, 4>(ma, mb, P, grid, stream);
-    if (BN == 128) return launch_cfg<128, 6>(ma, mb, P, grid, stream);
-    return launch_cfg<64, 8>(ma, mb, P, grid, stream);
+    cudaEvent_t ta = nullptr, tb = nullptr;
+    bool timed = false;
+    {
+        std::lock_guard<std::mutex> lk(timing().mu);
+        timed = timing().on;
+    }
+    if (timed) {
+        cudaEventCreate(&ta);
+        cudaEventCreate(&tb);
+        cudaEventRecord(ta, stream);
+    }
+    cudaError_t e;
+    if (BN == 256)
+        e = launch_cfg<256, 4>(ma, mb, P, grid, stream);
+    else if (BN == 128)
+        e = launch_cfg<128, 6>(ma, mb, P, grid, stream);
+    else
+        e = launch_cfg<64, 8>(ma, mb, P, grid, stream);
+    if (timed) {
+        cudaEventRecord(tb, stream);
+        std::lock_guard<std::mutex> lk(timing().mu);
+        timing().recs.push_back({ta, tb, executed_flops(g)});
+    }
+    return e;
 }
 
 }  // namespace gemm

@@ -7,6 +7,7 @@
 // offload plans reproduce bit-identical training state.
 #include "common.cuh"
 #include "gpt_kernels.h"
+#include "kernels.h"
 
 namespace ah {
 namespace gpt {
@@ -337,13 +338,13 @@ __global__ void loss_sum_kernel(const float* __restrict__ loss, int T, float* ou
 cudaError_t embed_fwd(const int* tok, const uint16_t* wte, const uint16_t* wpe, uint16_t* x, int T, int s, int h,
                       cudaStream_t st) {
     embed_fwd_kernel<<<T, 256, 0, st>>>(tok, wte, wpe, x, T, s, h);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean, float* rstd,
                    int T, int h, cudaStream_t st) {
     ln_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T, h);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 int ln_bwd_ctas(int T) { return T < 592 ? T : 592; }
@@ -366,7 +367,7 @@ cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, con
     }
     ln_bwd_kernel<<<ctas, warps * 32, sm, st>>>(dy, x, mean, rstd, g, dres, dx, part, T, h, rows);
     colsum_finish_kernel<<<(2 * h + 255) / 256, 256, 0, st>>>(part, ctas, 2 * h, dgdb, 0, nullptr);
-    return cudaGetLastError();
+    return launched(2);
 }
 
 int colsum_rows(int T) { return T >= 4096 ? 64 : (T >= 256 ? 16 : 1); }
@@ -377,50 +378,50 @@ cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* 
     dim3 grid((N / 8 + 127) / 128, R);
     colsum_partial_kernel<<<grid, 128, 0, st>>>(X, T, N, ldx, rows, part);
     colsum_finish_kernel<<<(N + 255) / 256, 256, 0, st>>>(part, R, N, out, out_f32, nullptr);
-    return cudaGetLastError();
+    return launched(2);
 }
 
 cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st) {
     softmax_fwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(S, P, rows, s);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st) {
     softmax_bwd_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(P, dP, dS, rows, s);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre, size_t n, cudaStream_t st) {
     const size_t n8 = n / 8;
     gelu_bwd_kernel<<<148 * 8, 256, 0, st>>>(dgelu, pre, dpre, n8);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
                           cudaStream_t st) {
     ce_kernel<<<T, 512, 0, st>>>(logits, tgt, loss, V, ld, dscale);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t embed_bwd_tok(const uint16_t* dx, const int* uniq, const int* offs, const int* pos, int n_uniq,
                           float* dwte, int h, cudaStream_t st) {
     if (n_uniq > 0) embed_bwd_tok_kernel<<<n_uniq, 256, 0, st>>>(dx, uniq, offs, pos, dwte, h);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t embed_bwd_pos(const uint16_t* dx, float* dwpe, int B, int s, int h, cudaStream_t st) {
     embed_bwd_pos_kernel<<<s, 256, 0, st>>>(dx, dwpe, B, s, h);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t f32_to_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st) {
     f32_to_bf16_kernel<<<148 * 8, 256, 0, st>>>(src, dst, n);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t mean_loss(const float* loss, int T, float* out, cudaStream_t st) {
     loss_sum_kernel<<<1, 1024, 0, st>>>(loss, T, out);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 }  // namespace gpt
@@ -449,11 +450,11 @@ __global__ void fill_kernel(float* p, size_t n, float v) {
 }  // namespace
 cudaError_t init_normal(float* p, size_t n, unsigned long long seed, float mean, float std, cudaStream_t st) {
     init_normal_kernel<<<148 * 8, 256, 0, st>>>(p, n, seed, mean, std);
-    return cudaGetLastError();
+    return launched(1);
 }
 cudaError_t fill_f32(float* p, size_t n, float v, cudaStream_t st) {
     fill_kernel<<<148 * 8, 256, 0, st>>>(p, n, v);
-    return cudaGetLastError();
+    return launched(1);
 }
 }  // namespace gpt
 }  // namespace ah
@@ -536,13 +537,13 @@ cudaError_t token_index(const int* tok, int T, int* uniq, int* offs, int* pos, i
         cfg = true;
     }
     token_index_kernel<<<1, 1024, sm, st>>>(tok, T, n2, uniq, offs, pos, n_uniq);
-    return cudaGetLastError();
+    return launched(1);
 }
 
 cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* offs, const int* pos,
                               const int* n_uniq, int T, float* dwte, int h, cudaStream_t st) {
     embed_bwd_tok_dev_kernel<<<T, 256, 0, st>>>(dx, uniq, offs, pos, n_uniq, dwte, h);
-    return cudaGetLastError();
+    return launched(1);
 }
 }  // namespace gpt
 }  // namespace ah

@@ -27,3 +27,16 @@ cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, floa
                               cudaStream_t stream);
 
 }  // namespace ah
+
+#include <atomic>
+namespace ah {
+// Number of kernels this library has launched (for the bench's gpu_launches claim).
+inline std::atomic<long long>& kernel_launch_counter() {
+    static std::atomic<long long> c{0};
+    return c;
+}
+inline cudaError_t launched(int n) {
+    kernel_launch_counter().fetch_add(n, std::memory_order_relaxed);
+    return cudaGetLastError();
+}
+}  // namespace ah

@@ -149,7 +149,7 @@ void Trainer::plan(const ah_trainer_config& cfg) {
     spec.vocab_size = d_.V;
     // Real activation bytes of a block (input + saved set) over the 2*b*s*h unit.
     spec.activation_coef = (double)(BlockActs::bytes(d_) + T * h * 2) / (double)(2 * T * h);
-    spec.bwd_fwd_ratio = 2.0;
+    spec.bwd_fwd_ratio = cfg.bwd_fwd_ratio > 0 ? cfg.bwd_fwd_ratio : 2.0;
     hw_.gpu_mem = cfg.gpu_mem_budget;
     hw_.cpu_mem = cfg.cpu_mem_budget;
     hw_.gpu_compute_rate = cfg.gpu_flops;
@@ -759,6 +759,125 @@ std::string Trainer::trace_json() {
     });
     hetsim::write_chrome_trace(out, ops);
     return out.str();
+}
+
+}  // namespace ah
+
+// ---------------------------------------------------------------------------------------
+// Runtime profiler (paper §3.1): one block measured on this box.
+// ---------------------------------------------------------------------------------------
+namespace ah {
+
+ah_hw_profile profile_block(const ah_trainer_config& cfg) {
+    GptDims d;
+    d.L = 1;
+    d.h = cfg.hidden;
+    d.nh = cfg.heads;
+    d.hd = cfg.hidden / cfg.heads;
+    d.s = cfg.seq_len;
+    d.B = cfg.batch;
+    d.V = cfg.vocab;
+    d.Vp = (int)round_up((size_t)cfg.vocab, 128);
+    const size_t mp = d.m_p(), T = d.T(), h = d.h;
+    auto ok = [](cudaError_t e, const char* w) {
+        if (e != cudaSuccess) throw std::runtime_error(std::string(w) + ": " + cudaGetErrorString(e));
+    };
+    cudaStream_t st;
+    ok(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    float *master, *m1, *m2;
+    uint16_t *w, *x0, *x1, *gx0, *gx1;
+    void *acts, *wsm;
+    ok(cudaMalloc(&master, mp * 4), "alloc");
+    ok(cudaMalloc(&m1, mp * 4), "alloc");
+    ok(cudaMalloc(&m2, mp * 4), "alloc");
+    ok(cudaMalloc(&w, mp * 2), "alloc");
+    for (uint16_t** p : {&x0, &x1, &gx0, &gx1}) ok(cudaMalloc(p, T * h * 2), "alloc");
+    ok(cudaMalloc(&acts, BlockActs::bytes(d)), "alloc");
+    ok(cudaMalloc(&wsm, Workspace::bytes(d)), "alloc");
+    const Workspace ws = Workspace::carve(d, wsm);
+    const BlockActs a = BlockActs::carve(d, acts);
+    ok(gpt::init_normal(master, mp, 99, 0.f, 0.02f, st), "init");
+    ok(cudaMemsetAsync(m1, 0, mp * 4, st), "memset");
+    ok(cudaMemsetAsync(m2, 0, mp * 4, st), "memset");
+    ok(launch_cast_f32_bf16(master, w, mp, st), "cast");
+    ok(cudaMemsetAsync(x0, 0, T * h * 2, st), "memset");
+    ok(cudaMemsetAsync(gx0, 0, T * h * 2, st), "memset");
+    cudaEvent_t e0, e1;
+    ok(cudaEventCreate(&e0), "event");
+    ok(cudaEventCreate(&e1), "event");
+    auto timed = [&](int reps, auto&& body) {
+        body();  // warm-up
+        ok(cudaStreamSynchronize(st), "sync");
+        ok(cudaEventRecord(e0, st), "record");
+        for (int r = 0; r < reps; ++r) body();
+        ok(cudaEventRecord(e1, st), "record");
+        ok(cudaEventSynchronize(e1), "sync");
+        float ms = 0.f;
+        ok(cudaEventElapsedTime(&ms, e0, e1), "elapsed");
+        return (double)ms / 1e3 / reps;
+    };
+    ah_hw_profile out{};
+    out.t_fwd_s = timed(5, [&] { ok(block_forward(d, w, x0, x1, a, ws, st), "fwd"); });
+    // backward consumes the weight slots as gradient storage: re-materialise each rep (cheap)
+    const double t_cast = timed(5, [&] { ok(launch_cast_f32_bf16(master, w, mp, st), "cast"); });
+    const double t_bwd_cast = timed(5, [&] {
+        ok(launch_cast_f32_bf16(master, w, mp, st), "cast");
+        ok(block_backward(d, w, x0, a, gx0, gx1, ws, st), "bwd");
+    });
+    out.t_bwd_s = t_bwd_cast - t_cast;
+    const double flops = 2.0 * (double)mp * (double)T + 4.0 * d.B * (double)d.s * d.s * h;
+    out.gpu_flops = flops / out.t_fwd_s;
+    out.bwd_fwd_ratio = out.t_bwd_s / out.t_fwd_s;
+    ah_adam_hparams hp = cfg.adam;
+    hp.step = 1;
+    const double t_adam = timed(5, [&] { ok(launch_adam(adam_args(hp, 1, master, m1, m2, w, nullptr, mp), st), "adam"); });
+    out.gpu_adam_rate = (double)mp / t_adam;
+    uint16_t* hbuf;
+    ok(cudaHostAlloc((void**)&hbuf, mp * 2, cudaHostAllocPortable), "host alloc");
+    std::memset(hbuf, 0, mp * 2);
+    out.h2d_bw = (double)mp * 2 / timed(5, [&] { ok(cudaMemcpyAsync(w, hbuf, mp * 2, cudaMemcpyHostToDevice, st), "h2d"); });
+    out.d2h_bw = (double)mp * 2 / timed(5, [&] { ok(cudaMemcpyAsync(hbuf, w, mp * 2, cudaMemcpyDeviceToHost, st), "d2h"); });
+    // CPU Adam on host copies of one block's state
+    float *hp_, *hm, *hv;
+    ok(cudaHostAlloc((void**)&hp_, mp * 4, cudaHostAllocPortable), "host alloc");
+    ok(cudaHostAlloc((void**)&hm, mp * 4, cudaHostAllocPortable), "host alloc");
+    ok(cudaHostAlloc((void**)&hv, mp * 4, cudaHostAllocPortable), "host alloc");
+    std::memset(hp_, 0, mp * 4);
+    std::memset(hm, 0, mp * 4);
+    std::memset(hv, 0, mp * 4);
+    cpu_adam(hp, hp_, hm, hv, hbuf, hbuf, mp, 1.f, cfg.cpu_threads);  // warm-up / page-in
+    const auto c0 = Clock::now();
+    const int reps = 3;
+    for (int r = 0; r < reps; ++r) cpu_adam(hp, hp_, hm, hv, hbuf, hbuf, mp, 1.f, cfg.cpu_threads);
+    const double tc = std::chrono::duration<double>(Clock::now() - c0).count() / reps;
+    out.cpu_adam_rate = (double)mp / tc;
+    cudaFreeHost(hp_);
+    cudaFreeHost(hm);
+    cudaFreeHost(hv);
+    cudaFreeHost(hbuf);
+    for (void* p : {(void*)master, (void*)m1, (void*)m2, (void*)w, (void*)x0, (void*)x1, (void*)gx0, (void*)gx1, acts, wsm})
+        cudaFree(p);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaStreamDestroy(st);
+    return out;
+}
+
+float Trainer::timer(bool stop) {
+    drain();
+    if (!timer_ev_[0]) {
+        check(cudaEventCreate(&timer_ev_[0]), "event");
+        check(cudaEventCreate(&timer_ev_[1]), "event");
+    }
+    if (!stop) {
+        check(cudaEventRecord(timer_ev_[0], s_compute_), "record");
+        return 0.f;
+    }
+    check(cudaEventRecord(timer_ev_[1], s_compute_), "record");
+    check(cudaEventSynchronize(timer_ev_[1]), "sync");
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, timer_ev_[0], timer_ev_[1]), "elapsed");
+    return ms;
 }
 
 }  // namespace ah

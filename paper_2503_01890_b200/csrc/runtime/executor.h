@@ -55,8 +55,11 @@ public:
     size_t master_size(int block) const;
     // Chrome trace of the last drained iterations in the reference schema (simulator.cpp:598).
     std::string trace_json();
+    // drain + record start (stop=false) / drain + record stop and return elapsed ms (stop=true)
+    float timer(bool stop);
 
 private:
+    cudaEvent_t timer_ev_[2] = {nullptr, nullptr};
     enum Lane { kCompute = 0, kH2D = 1, kD2H = 2, kCpu = 3 };
     struct OpKey {
         int kind, block;

@@ -44,6 +44,7 @@ class PlanConfig:
     d2h_bw: float = 50e9
     cpu_adam_rate: float = 1.0e9
     gpu_adam_rate: float = 2.0e11
+    bwd_fwd_ratio: float = 2.0
 
 
 @dataclasses.dataclass
@@ -74,6 +75,7 @@ class Trainer:
         cfg.gpu_mem_budget, cfg.cpu_mem_budget = plan.gpu_mem_budget, plan.cpu_mem_budget
         cfg.gpu_flops, cfg.h2d_bw, cfg.d2h_bw = plan.gpu_flops, plan.h2d_bw, plan.d2h_bw
         cfg.cpu_adam_rate, cfg.gpu_adam_rate = plan.cpu_adam_rate, plan.gpu_adam_rate
+        cfg.bwd_fwd_ratio = plan.bwd_fwd_ratio
         cfg.adam = N.AdamHParams(adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, 1)
         cfg.seed = seed
         cfg.cpu_threads = cpu_threads
@@ -140,6 +142,11 @@ class Trainer:
         N.check(N.lib().ah_trainer_read_master(self._h, block, out.ctypes.data, n), "ah_trainer_read_master")
         return out
 
+    def timer(self, stop: bool) -> float:
+        ms = C.c_float()
+        N.check(N.lib().ah_trainer_timer(self._h, int(stop), C.byref(ms)), "ah_trainer_timer")
+        return ms.value
+
     def trace(self) -> list:
         n = N.lib().ah_trainer_trace(self._h, None, 0)
         if n < 0:
@@ -147,3 +154,21 @@ class Trainer:
         buf = C.create_string_buffer(max(n, 1) + 4096)
         N.check(min(0, N.lib().ah_trainer_trace(self._h, buf, len(buf))), "ah_trainer_trace")
         return json.loads(buf.value.decode())
+
+
+def profile_hardware(model: ModelConfig, cpu_threads: int = 0) -> dict:
+    """Runtime profiler (paper §3.1): measure one block on this GPU/host -> planner rates."""
+    cfg = N.TrainerConfig()
+    for f in dataclasses.fields(model):
+        setattr(cfg, f.name, getattr(model, f.name))
+    cfg.adam = N.AdamHParams(1e-4, 0.9, 0.999, 1e-8, 0.01, 1)
+    cfg.cpu_threads = cpu_threads
+    out = N.HwProfile()
+    N.check(N.lib().ah_profile_block(C.byref(cfg), C.byref(out)), "ah_profile_block")
+    return {f: getattr(out, f) for f, _ in out._fields_}
+
+
+def plan_from_profile(prof: dict, gpu_mem_budget: int, cpu_mem_budget: int, **kw) -> PlanConfig:
+    return PlanConfig(gpu_mem_budget=gpu_mem_budget, cpu_mem_budget=cpu_mem_budget, gpu_flops=prof["gpu_flops"],
+                      h2d_bw=prof["h2d_bw"], d2h_bw=prof["d2h_bw"], cpu_adam_rate=prof["cpu_adam_rate"],
+                      gpu_adam_rate=prof["gpu_adam_rate"], bwd_fwd_ratio=prof["bwd_fwd_ratio"], **kw)
