@@ -181,12 +181,19 @@ def main():
 
     model = ModelConfig(**m)
     prof = profile_hardware(model, cpu_threads=a.cpu_threads)
+    nccl_id = None
+    if dist:
+        # every rank must plan identically (same collective order): use rank 0's rates
+        obj = [prof, N.dp_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        prof, nccl_id = obj
     kw = {}
     if a.strategy:
         c, p, o = (int(x) for x in a.strategy.split(","))
         kw = dict(c_hat=c, p_hat=p, o_hat=o)
     plan = plan_from_profile(prof, a.gpu_mem_gib << 30, a.cpu_mem_gib << 30, **kw)
-    tr = Trainer(model, plan, seed=1234 + rank, cpu_threads=a.cpu_threads)
+    # replicas start from identical weights (seed shared); data differs per rank
+    tr = Trainer(model, plan, seed=1234, cpu_threads=a.cpu_threads, dp_rank=rank, dp_size=world, nccl_id=nccl_id)
     st0 = tr.stats()
 
     T = m["batch"] * m["seq_len"]

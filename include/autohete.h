@@ -153,7 +153,21 @@ typedef struct ah_trainer_config {
     ah_adam_hparams adam;
     uint64_t seed;
     int32_t cpu_threads; /* CPU Adam threads, <= 0 = all */
+    /* Data parallel (north_star (d)): dp_size ranks, one per GPU; each rank owns a 1/dp_size
+     * shard of every block's fp32 master + moments (GPU or pinned host per the plan).
+     * Parameters are all-gathered (bf16) before each use, gradients reduce-scattered
+     * (bf16 sum, 1/dp_size folded into the optimizer) after each block's backward — NCCL over
+     * NVLink, issued in the compute lane's deterministic order. dp_size <= 1 and
+     * !force_collectives => no NCCL. nccl_id: ncclUniqueId from ah_dp_unique_id on rank 0. */
+    int32_t dp_rank, dp_size, force_collectives;
+    uint8_t nccl_id[128];
 } ah_trainer_config;
+
+/* ncclGetUniqueId into out[128] (rank 0; broadcast it to the other ranks). */
+int ah_dp_unique_id(uint8_t* out);
+/* Shard of a flat block vector of n elements owned by `rank` (16-byte aligned shards):
+ * elements [*offset, *offset + *len) of the padded vector of dp_size * (*shard) elements. */
+int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard);
 
 typedef struct ah_trainer_stats {
     int32_t c_hat, p_hat, o_hat;

@@ -129,6 +129,8 @@ class TrainerConfig(C.Structure):
         ("gpu_flops", C.c_double), ("h2d_bw", C.c_double), ("d2h_bw", C.c_double),
         ("cpu_adam_rate", C.c_double), ("gpu_adam_rate", C.c_double), ("bwd_fwd_ratio", C.c_double),
         ("adam", AdamHParams), ("seed", C.c_uint64), ("cpu_threads", C.c_int32),
+        ("dp_rank", C.c_int32), ("dp_size", C.c_int32), ("force_collectives", C.c_int32),
+        ("nccl_id", C.c_uint8 * 128),
     ]
 
 
@@ -170,3 +172,22 @@ _EXTRA_SIGS.update({
     "ah_kernel_launches": ([], C.c_int64),
     "ah_gemm_timing": ([C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
 })
+
+_EXTRA_SIGS.update({
+    "ah_dp_unique_id": ([C.c_void_p], C.c_int),
+    "ah_dp_shard": ([C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                     C.POINTER(C.c_int64)], C.c_int),
+})
+
+
+def dp_unique_id() -> bytes:
+    buf = (C.c_uint8 * 128)()
+    check(lib().ah_dp_unique_id(buf), "ah_dp_unique_id")
+    return bytes(buf)
+
+
+def dp_shard(n: int, rank: int, size: int) -> tuple[int, int, int]:
+    """(offset, valid length, padded shard length) of rank's shard of an n-element block vector."""
+    off, ln, sh = C.c_int64(), C.c_int64(), C.c_int64()
+    check(lib().ah_dp_shard(n, rank, size, C.byref(off), C.byref(ln), C.byref(sh)), "ah_dp_shard")
+    return off.value, ln.value, sh.value

@@ -16,6 +16,7 @@ import glob
 import os
 import shutil
 import subprocess
+import sysconfig
 import sys
 
 PKG = os.path.dirname(os.path.abspath(__file__))
@@ -26,8 +27,8 @@ OBJ = os.path.join(PKG, "build", "obj")
 INC = os.path.join(ROOT, "include")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
-SITE = os.path.dirname(os.path.dirname(os.__file__))
-NCCL_HOME = os.path.join(SITE, "site-packages", "nvidia", "nccl")
+SITE = sysconfig.get_paths()["purelib"]
+NCCL_HOME = os.path.join(SITE, "nvidia", "nccl")  # torch-bundled NCCL 2.28.9 (headers + lib)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXSTD = "-std=c++20"

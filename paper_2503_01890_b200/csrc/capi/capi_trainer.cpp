@@ -136,3 +136,29 @@ int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out) {
 }
 
 }  // extern "C"
+
+#include <nccl.h>
+
+extern "C" {
+
+int ah_dp_unique_id(uint8_t* out) {
+    if (!out) return ah::set_error(AH_ERR_INVALID, "ah_dp_unique_id: null out");
+    ncclUniqueId id;
+    const ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return ah::set_error(AH_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    std::memcpy(out, &id, sizeof(id));
+    return AH_OK;
+}
+
+int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard) {
+    if (n < 0 || dp_size < 1 || rank < 0 || rank >= dp_size || !offset || !len || !shard)
+        return ah::set_error(AH_ERR_INVALID, "ah_dp_shard: bad argument");
+    const int64_t per = ((n + dp_size - 1) / dp_size + 7) / 8 * 8;
+    const int64_t off = per * rank;
+    *shard = per;
+    *offset = off;
+    *len = off >= n ? 0 : (n - off < per ? n - off : per);
+    return AH_OK;
+}
+
+}  // extern "C"

@@ -15,6 +15,8 @@
 #include "hetsim/costmodel.hpp"
 #include "hetsim/workload.hpp"
 
+#include <nccl.h>
+
 namespace ah {
 
 void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uint16_t* g, uint16_t* p_bf16,
@@ -80,6 +82,22 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     seed_ = cfg.seed ? cfg.seed : 1234;
     cpu_threads_ = cfg.cpu_threads;
     ps_ = cfg.priority_sched != 0;
+    dp_rank_ = cfg.dp_rank;
+    dp_size_ = cfg.dp_size < 1 ? 1 : cfg.dp_size;
+    dp_ = dp_size_ > 1 || cfg.force_collectives;
+    if (dp_rank_ < 0 || dp_rank_ >= dp_size_) throw std::invalid_argument("trainer: dp_rank out of range");
+    if (dp_) {
+        shard_ = round_up((d_.m_p() + dp_size_ - 1) / dp_size_, 8);
+        const size_t off = shard_ * (size_t)dp_rank_;
+        my_len_ = off >= d_.m_p() ? 0 : std::min(shard_, d_.m_p() - off);
+        ncclUniqueId id;
+        static_assert(sizeof(id) == 128, "ncclUniqueId size");
+        std::memcpy(&id, cfg.nccl_id, sizeof(id));
+        ncclComm_t comm;
+        const ncclResult_t r = ncclCommInitRank(&comm, dp_size_, id, dp_rank_);
+        if (r != ncclSuccess) throw std::runtime_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        comm_ = comm;
+    }
     int lo = 0, hi = 0;
     check(cudaDeviceGetStreamPriorityRange(&lo, &hi), "priority range");
     check(cudaStreamCreateWithPriority(&s_compute_, cudaStreamNonBlocking, hi), "stream");
@@ -99,6 +117,7 @@ Trainer::~Trainer() {
     for (auto& t : lanes_)
         if (t.joinable()) t.join();
     cudaDeviceSynchronize();
+    if (comm_) ncclCommDestroy(static_cast<ncclComm_t>(comm_));
     for (Iter* it : iters_) {
         for (auto& kv : it->ops) {
             RtOp& o = kv.second;
@@ -245,25 +264,34 @@ void Trainer::allocate_and_init() {
         check(gpt::fill_f32(tmp + lay.ln1_b, h, 0.f, st), "init");
         check(gpt::fill_f32(tmp + lay.ln2_g, h, 1.f, st), "init");
         check(gpt::fill_f32(tmp + lay.ln2_b, h, 0.f, st), "init");
+        // this rank's part of the fp32 state: the whole block, or its DP shard (zero padded)
+        const size_t n = dp_ ? shard_ : mp;
+        const size_t off = dp_ ? shard_ * (size_t)dp_rank_ : 0;
+        const size_t valid = dp_ ? my_len_ : mp;
         if (b.o) {
             // optimizer state in pinned host DRAM: 12 B/param + shared 2 B param/grad buffer
-            check(cudaHostAlloc((void**)&b.master, mp * 4, cudaHostAllocPortable), "host alloc");
-            check(cudaHostAlloc((void**)&b.m1, mp * 4, cudaHostAllocPortable), "host alloc");
-            check(cudaHostAlloc((void**)&b.m2, mp * 4, cudaHostAllocPortable), "host alloc");
-            check(cudaHostAlloc((void**)&b.host_bf16, mp * 2, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.master, n * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.m1, n * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.m2, n * 4, cudaHostAllocPortable), "host alloc");
+            check(cudaHostAlloc((void**)&b.host_bf16, n * 2, cudaHostAllocPortable), "host alloc");
+            std::memset(b.master, 0, n * 4);
+            std::memset(b.host_bf16, 0, n * 2);
             check(launch_cast_f32_bf16(tmp, tmpb, mp, st), "cast");
-            check(cudaMemcpyAsync(b.master, tmp, mp * 4, cudaMemcpyDeviceToHost, st), "copy");
-            check(cudaMemcpyAsync(b.host_bf16, tmpb, mp * 2, cudaMemcpyDeviceToHost, st), "copy");
+            if (valid) {
+                check(cudaMemcpyAsync(b.master, tmp + off, valid * 4, cudaMemcpyDeviceToHost, st), "copy");
+                check(cudaMemcpyAsync(b.host_bf16, tmpb + off, valid * 2, cudaMemcpyDeviceToHost, st), "copy");
+            }
             check(cudaStreamSynchronize(st), "sync");
-            std::memset(b.m1, 0, mp * 4);
-            std::memset(b.m2, 0, mp * 4);
+            std::memset(b.m1, 0, n * 4);
+            std::memset(b.m2, 0, n * 4);
         } else {
-            dalloc((void**)&b.master, mp * 4);
-            dalloc((void**)&b.m1, mp * 4);
-            dalloc((void**)&b.m2, mp * 4);
-            check(cudaMemcpyAsync(b.master, tmp, mp * 4, cudaMemcpyDeviceToDevice, st), "copy");
-            check(cudaMemsetAsync(b.m1, 0, mp * 4, st), "memset");
-            check(cudaMemsetAsync(b.m2, 0, mp * 4, st), "memset");
+            dalloc((void**)&b.master, n * 4);
+            dalloc((void**)&b.m1, n * 4);
+            dalloc((void**)&b.m2, n * 4);
+            check(cudaMemsetAsync(b.master, 0, n * 4, st), "memset");
+            if (valid) check(cudaMemcpyAsync(b.master, tmp + off, valid * 4, cudaMemcpyDeviceToDevice, st), "copy");
+            check(cudaMemsetAsync(b.m1, 0, n * 4, st), "memset");
+            check(cudaMemsetAsync(b.m2, 0, n * 4, st), "memset");
         }
     }
     check(cudaStreamSynchronize(st), "sync");
@@ -485,12 +513,22 @@ void Trainer::embed_backward_and_update(Iter& it) {
     check(gpt::embed_bwd_tok_dev(dx0, uniq, offs, pos, nuniq, T, dwte_, h, st), "embed bwd");
     check(gpt::embed_bwd_pos(dx0, dwpe_, d_.B, d_.s, h, st), "pos bwd");
     const size_t nwte = (size_t)d_.Vp * h, nwpe = (size_t)d_.s * h;
+    if (dp_) {  // replicated embedding / positions / final LN: sum gradients over ranks
+        dp_allreduce_f32(dwte_, nwte, st);
+        dp_allreduce_f32(dwpe_, nwpe, st);
+        dp_allreduce_bf16(dlnf_b_, 2 * (size_t)h, st);
+    }
     check(gpt::f32_to_bf16(dwte_, dwte_b_, nwte, st), "cvt");
     check(gpt::f32_to_bf16(dwpe_, dwpe_b_, nwpe, st), "cvt");
     const int step = (int)it.k;
-    check(launch_adam(adam_args(adam_, step, wte_, wte_m_, wte_v_, dwte_b_, wte_b_, nwte), st), "adam wte");
-    check(launch_adam(adam_args(adam_, step, wpe_, wpe_m_, wpe_v_, dwpe_b_, wpe_b_, nwpe), st), "adam wpe");
-    check(launch_adam(adam_args(adam_, step, lnf_, lnf_m_, lnf_v_, dlnf_b_, lnf_b_, 2 * (size_t)h), st), "adam lnf");
+    const float inv = 1.f / (float)dp_size_;
+    AdamArgs a1 = adam_args(adam_, step, wte_, wte_m_, wte_v_, dwte_b_, wte_b_, nwte);
+    AdamArgs a2 = adam_args(adam_, step, wpe_, wpe_m_, wpe_v_, dwpe_b_, wpe_b_, nwpe);
+    AdamArgs a3 = adam_args(adam_, step, lnf_, lnf_m_, lnf_v_, dlnf_b_, lnf_b_, 2 * (size_t)h);
+    a1.inv_scale = a2.inv_scale = a3.inv_scale = inv;
+    check(launch_adam(a1, st), "adam wte");
+    check(launch_adam(a2, st), "adam wpe");
+    check(launch_adam(a3, st), "adam lnf");
 }
 
 void Trainer::run_compute(Iter& it, RtOp& op) {
@@ -498,10 +536,20 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
     BlockState& b = blocks_[(size_t)i];
     cudaStream_t st = s_compute_;
     const size_t mp = d_.m_p();
+    const size_t off = shard_ * (size_t)dp_rank_;
     auto materialize = [&]() {  // bf16 weights from the on-GPU fp32 master (footnote 2)
-        check(cudaMallocAsync((void**)&b.wbuf, mp * 2, st), "alloc wbuf");
-        check(launch_cast_f32_bf16(b.master, b.wbuf, mp, st), "cast");
+        check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, st), "alloc wbuf");
+        if (dp_) {  // own shard, then all-gather the others over NVLink
+            check(launch_cast_f32_bf16(b.master, b.wbuf + off, shard_, st), "cast");
+            dp_gather(b.wbuf, st);
+        } else {
+            check(launch_cast_f32_bf16(b.master, b.wbuf, mp, st), "cast");
+        }
     };
+    if (b.needs_gather && op.kind != OpKind::GpuOptim) {  // prefetched shard -> full weights
+        dp_gather(b.wbuf, st);
+        b.needs_gather = false;
+    }
     auto alloc_acts = [&]() { check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts"); };
     auto free_acts = [&]() {
         check(cudaFreeAsync(b.acts, st), "free acts");
@@ -537,11 +585,18 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             check(block_backward(d_, b.wbuf, x_[(size_t)i - 1], a, gx_[i & 1], gx_[(i - 1) & 1], ws_, st),
                   "block bwd");
             free_acts();
+            if (dp_) {  // full local grads -> this rank's reduced shard (in place)
+                if (full_len() > mp) check(cudaMemsetAsync(b.wbuf + mp, 0, (full_len() - mp) * 2, st), "pad");
+                dp_reduce_grads(b.wbuf, st);
+            }
             if (i == 1) embed_backward_and_update(it);
             break;
         }
         case OpKind::GpuOptim: {
-            check(launch_adam(adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf, nullptr, mp), st), "adam");
+            AdamArgs aa = dp_ ? adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf + off, nullptr, shard_)
+                              : adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf, nullptr, mp);
+            aa.inv_scale = 1.f / (float)dp_size_;
+            check(launch_adam(aa, st), "adam");
             free_wbuf();
             break;
         }
@@ -554,18 +609,25 @@ void Trainer::run_h2d(Iter& it, RtOp& op) {
     (void)it;
     BlockState& b = blocks_[(size_t)op.block];
     const size_t mp = d_.m_p();
-    check(cudaMallocAsync((void**)&b.wbuf, mp * 2, s_h2d_), "alloc prefetch");
+    const size_t n = dp_ ? shard_ : mp;  // DP: only this rank's shard crosses the host link
+    uint16_t* dst = nullptr;
+    check(cudaMallocAsync((void**)&dst, full_len() * 2, s_h2d_), "alloc prefetch");
+    uint16_t* mine = dp_ ? dst + shard_ * (size_t)dp_rank_ : dst;
     if (b.o)
-        check(cudaMemcpyAsync(b.wbuf, b.host_bf16, mp * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
+        check(cudaMemcpyAsync(mine, b.host_bf16, n * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
     else  // P\O backward prefetch: the fp32 master is on the GPU; materialise without PCIe
-        check(launch_cast_f32_bf16(b.master, b.wbuf, mp, s_h2d_), "prefetch cast");
+        check(launch_cast_f32_bf16(b.master, mine, n, s_h2d_), "prefetch cast");
+    std::lock_guard<std::mutex> lk(mu_);
+    b.wbuf = dst;
+    b.needs_gather = dp_;  // the compute lane all-gathers before first use (deterministic order)
 }
 
 void Trainer::run_d2h(Iter& it, RtOp& op) {
     (void)it;
     BlockState& b = blocks_[(size_t)op.block];
-    const size_t mp = d_.m_p();
-    check(cudaMemcpyAsync(b.host_bf16, b.wbuf, mp * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
+    const size_t n = dp_ ? shard_ : d_.m_p();
+    const uint16_t* src = dp_ ? b.wbuf + shard_ * (size_t)dp_rank_ : b.wbuf;
+    check(cudaMemcpyAsync(b.host_bf16, src, n * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
     check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
     b.wbuf = nullptr;
 }
@@ -575,8 +637,31 @@ void Trainer::run_cpu(Iter& it, RtOp& op) {
     ah_adam_hparams hp = adam_;
     hp.step = (int)it.k;
     const auto t0 = Clock::now();
-    cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, d_.m_p(), 1.f, cpu_threads_);
+    const size_t n = dp_ ? shard_ : d_.m_p();
+    cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);
     op.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+void Trainer::dp_gather(uint16_t* wbuf, cudaStream_t st) {
+    const ncclResult_t r = ncclAllGather(wbuf + shard_ * (size_t)dp_rank_, wbuf, shard_, ncclBfloat16,
+                                         static_cast<ncclComm_t>(comm_), st);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+}
+
+void Trainer::dp_reduce_grads(uint16_t* wbuf, cudaStream_t st) {
+    const ncclResult_t r = ncclReduceScatter(wbuf, wbuf + shard_ * (size_t)dp_rank_, shard_, ncclBfloat16, ncclSum,
+                                             static_cast<ncclComm_t>(comm_), st);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclReduceScatter: ") + ncclGetErrorString(r));
+}
+
+void Trainer::dp_allreduce_f32(float* p, size_t n, cudaStream_t st) {
+    const ncclResult_t r = ncclAllReduce(p, p, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), st);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+}
+
+void Trainer::dp_allreduce_bf16(uint16_t* p, size_t n, cudaStream_t st) {
+    const ncclResult_t r = ncclAllReduce(p, p, n, ncclBfloat16, ncclSum, static_cast<ncclComm_t>(comm_), st);
+    if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -687,7 +772,7 @@ float Trainer::step(const int32_t* tokens, const int32_t* targets) {
 }
 
 size_t Trainer::master_size(int block) const {
-    if (block >= 1 && block <= d_.L) return d_.m_p();
+    if (block >= 1 && block <= d_.L) return dp_ ? shard_ : d_.m_p();  // DP: this rank's shard
     if (block == 0) return (size_t)d_.Vp * d_.h;
     if (block == -1) return (size_t)d_.s * d_.h;
     if (block == -2) return 2 * (size_t)d_.h;
@@ -731,8 +816,9 @@ void Trainer::stats(ah_trainer_stats* s) {
         s->lane_busy_ms[l] = lane_stats_[l].busy_ms;
         s->lane_ops[l] = lane_stats_[l].ops;
     }
-    s->h2d_bytes = (int64_t)2 * profile_.block.m_p * (strategy_.o_hat + std::max(0, strategy_.p_hat));
-    s->d2h_bytes = (int64_t)2 * profile_.block.m_p * strategy_.o_hat;
+    const int64_t per_block = dp_ ? (int64_t)shard_ : profile_.block.m_p;  // host-link elements
+    s->h2d_bytes = 2 * per_block * (strategy_.o_hat + std::max(0, strategy_.p_hat));
+    s->d2h_bytes = 2 * per_block * strategy_.o_hat;
 }
 
 std::string Trainer::trace_json() {

@@ -60,6 +60,17 @@ public:
 
 private:
     cudaEvent_t timer_ev_[2] = {nullptr, nullptr};
+    // data parallel
+    int dp_rank_ = 0, dp_size_ = 1;
+    bool dp_ = false;      // collectives on
+    void* comm_ = nullptr; // ncclComm_t
+    size_t shard_ = 0;     // per-rank shard length of a block vector (elements, padded)
+    size_t my_len_ = 0;    // valid elements of this rank's shard
+    size_t full_len() const { return dp_ ? shard_ * (size_t)dp_size_ : d_.m_p(); }
+    void dp_gather(uint16_t* wbuf, cudaStream_t st);     // shard -> full bf16 weights
+    void dp_reduce_grads(uint16_t* wbuf, cudaStream_t st);  // full grads -> my shard (sum)
+    void dp_allreduce_f32(float* p, size_t n, cudaStream_t st);
+    void dp_allreduce_bf16(uint16_t* p, size_t n, cudaStream_t st);
     enum Lane { kCompute = 0, kH2D = 1, kD2H = 2, kCpu = 3 };
     struct OpKey {
         int kind, block;
@@ -99,6 +110,7 @@ private:
         uint16_t* host_bf16 = nullptr;  // O blocks: shared param/grad buffer
         uint16_t* wbuf = nullptr;       // device bf16 weights / grads while resident
         void* acts = nullptr;           // device activation set while live
+        bool needs_gather = false;      // DP: wbuf holds only this rank's shard so far
     };
 
     void plan(const ah_trainer_config& cfg);

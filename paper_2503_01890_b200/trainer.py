@@ -58,7 +58,10 @@ class AdamConfig:
 
 class Trainer:
     def __init__(self, model: ModelConfig, plan: PlanConfig | None = None, adam: AdamConfig | None = None,
-                 seed: int = 1234, cpu_threads: int = 0):
+                 seed: int = 1234, cpu_threads: int = 0, dp_rank: int = 0, dp_size: int = 1,
+                 nccl_id: bytes | None = None, force_collectives: bool = False):
+        """dp_size > 1: data parallel over NCCL; every rank passes the same nccl_id (from
+        _native.dp_unique_id() on rank 0) and the same seed / plan."""
         plan = plan or PlanConfig()
         adam = adam or AdamConfig()
         self.model = model
@@ -79,6 +82,10 @@ class Trainer:
         cfg.adam = N.AdamHParams(adam.lr, adam.beta1, adam.beta2, adam.eps, adam.weight_decay, 1)
         cfg.seed = seed
         cfg.cpu_threads = cpu_threads
+        cfg.dp_rank, cfg.dp_size, cfg.force_collectives = dp_rank, dp_size, int(force_collectives)
+        if dp_size > 1 or force_collectives:
+            nid = nccl_id if nccl_id is not None else N.dp_unique_id()
+            C.memmove(cfg.nccl_id, nid, 128)
         self._h = C.c_void_p()
         N.check(N.lib().ah_trainer_create(C.byref(cfg), C.byref(self._h)), "ah_trainer_create")
 

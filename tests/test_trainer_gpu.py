@@ -12,10 +12,10 @@ pytestmark = pytest.mark.gpu
 MODEL = dict(num_blocks=4, hidden=256, heads=2, seq_len=256, batch=2, vocab=1000)
 
 
-def make(plan=None, adam=None, seed=7):
+def make(plan=None, adam=None, seed=7, force_collectives=False):
     from paper_2503_01890_b200.trainer import AdamConfig, ModelConfig, PlanConfig, Trainer
     return Trainer(ModelConfig(**MODEL), plan or PlanConfig(c_hat=0, p_hat=0, o_hat=0),
-                   adam or AdamConfig(), seed=seed, cpu_threads=4)
+                   adam or AdamConfig(), seed=seed, cpu_threads=4, force_collectives=force_collectives)
 
 
 def batch(seed=0):
@@ -64,9 +64,10 @@ PLANS = [
 ]
 
 
-def run_plan(plan_kw, ps=True, steps=3):
+def run_plan(plan_kw, ps=True, steps=3, fc=False):
     from paper_2503_01890_b200.trainer import PlanConfig
-    tr = make(plan=PlanConfig(priority_sched=ps, fine_tune=False, gpu_mem_budget=1 << 40, **plan_kw))
+    tr = make(plan=PlanConfig(priority_sched=ps, fine_tune=False, gpu_mem_budget=1 << 40, **plan_kw),
+              force_collectives=fc)
     losses = []
     for k in range(steps):
         toks, tgts = batch(k)
@@ -107,3 +108,16 @@ def test_realised_lane_order_matches_scheduler(cuda_device, native):
         assert n > 0
         assert got[-n:] == want, (lane, got[-n:], want)
     tr.close()
+
+
+def test_dp_collective_path_is_exact_on_one_rank(cuda_device, native):
+    """The NCCL data-parallel path (shard, all-gather before use, reduce-scatter after the
+    backward, sharded GPU/CPU AdamW) on a 1-rank communicator reproduces the plain path bit
+    for bit, for an all-GPU and an offloading plan."""
+    base_loss, base_state, _ = run_plan(PLANS[0])
+    for plan in (PLANS[0], PLANS[3]):
+        loss, state, _ = run_plan(plan, fc=True)
+        assert loss == base_loss
+        for a, b in zip(state, base_state):
+            n = min(a.size, b.size)  # DP shard is padded to a multiple of 8
+            assert np.array_equal(a[:n].view(np.uint32), b[:n].view(np.uint32)), plan
