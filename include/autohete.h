@@ -102,6 +102,7 @@ int ah_stream_destroy(void* stream);
 #define AH_EPI_GELU 2
 #define AH_EPI_RESIDUAL 4
 #define AH_EPI_AUX 16
+#define AH_EPI_GELU_BWD 32 /* multiply by GELU'(aux): fused GELU backward */
 #define AH_CAUSAL_NONE 0
 #define AH_CAUSAL_SKIP_UPPER 1
 #define AH_CAUSAL_K_UPTO_M 2

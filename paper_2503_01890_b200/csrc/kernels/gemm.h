@@ -12,6 +12,7 @@ enum Epilogue : int {
     kEpiGelu = 2,      // tanh-GELU (GPT-2)
     kEpiResidual = 4,  // + residual[m, n] (bf16)
     kEpiAux = 16,      // store the pre-GELU value to aux (bf16)
+    kEpiGeluBwd = 32,  // multiply by GELU'(aux[m, n]) (aux = pre-activation, bf16)
 };
 
 enum Causal : int {

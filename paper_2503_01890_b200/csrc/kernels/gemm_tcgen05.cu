@@ -38,7 +38,11 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / spare; 4-11: epilogue
+constexpr int kEpiWarps = 8;
+// The smem-transposed (staged) epilogue is compiled but disabled: with 8 epilogue warps its
+// staging slabs do not fit beside a 4-stage BN=256 ring. Direct row stores are used.
+constexpr int kStagedSmem = 0;
 
 struct Params {
     int M, N, K;
@@ -57,7 +61,10 @@ struct Params {
     float alpha, beta;
     int epi;
     int causal;
-    int vec_c, vec_aux;  // 16-byte aligned rows => vector stores
+    int vec_c, vec_aux;      // 4-element vector access legal (staged path)
+    int vec16_c, vec16_aux;  // 16-byte rows (direct path)
+    int staged;              // smem-transposed epilogue (fp32 outputs)
+    int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
 };
 
 // ---------------------------------------------------------------------------------------
@@ -135,9 +142,28 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint3
     return d;
 }
 
+__device__ __forceinline__ float tanh_fast(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// v[base .. base+8) += 8 bf16 values packed in w
+__device__ __forceinline__ void add8(float (&v)[32], int base, uint4 w) {
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[base + e] += bf16_bits_to_f32((e & 1) ? (u[e >> 1] >> 16) : (u[e >> 1] & 0xffffu));
+}
+
+__device__ __forceinline__ float gelu_grad(float x) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const float th = tanh_fast(k0 * (x + k1 * x * x * x));
+    return 0.5f * (1.f + th) + 0.5f * x * (1.f - th * th) * k0 * (1.f + 3.f * k1 * x * x);
+}
+
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
-    return 0.5f * x * (1.f + tanhf(k0 * (x + k1 * x * x * x)));
+    return 0.5f * x * (1.f + tanh_fast(k0 * (x + k1 * x * x * x)));
 }
 
 struct Tile {
@@ -200,7 +226,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull[a]), 1);
-            mbar_init(smem_u32(&tempty[a]), 4);
+            mbar_init(smem_u32(&tempty[a]), kEpiWarps);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -297,8 +323,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
     } else if (warp >= 4) {
         // ===== epilogue =====
-        const int q = warp & 3;  // TMEM lane quarter
-        const int r = q * 32 + lane;
+        // TMEM -> registers (thread = row, 32 columns) -> per-warp smem slab -> each lane
+        // re-reads 4 consecutive columns of a row, so a warp instruction covers 4 rows x 32
+        // columns (128 B fp32 / 64 B bf16 per row). The element-wise epilogue runs in this
+        // phase: bias / residual / aux / C accesses are row-contiguous too.
+        // two warps per TMEM lane quarter (one per half of the tile's 32-column chunks): two
+        // epilogue warps per SM sub-partition, so the per-element work has the ILP to hide
+        // under the next tile's MMAs
+        const int q = warp & 3;  // TMEM lane quarter = 32-row slab of the tile
+        const int half = (warp - 4) >> 2;
+        float* stage = reinterpret_cast<float*>(tmem_holder + 4) + (warp - 4) * 32 * 36;
+        const int sub = lane & 7, rsub = lane >> 3;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
@@ -306,15 +341,21 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             if (T.skip) continue;
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
-            const int m = T.tm * BM + r;
-            const bool row_ok = m < P.M;
-            const long long c_off = (long long)T.z1 * P.c_s1 + (long long)T.z2 * P.c_s2 + (long long)m * P.ldc;
+            const int m_base = T.tm * BM + q * 32;
+            const long long zc = (long long)T.z1 * P.c_s1 + (long long)T.z2 * P.c_s2;
+            const long long zr = (long long)T.z1 * P.res_s1 + (long long)T.z2 * P.res_s2;
+            const long long za = (long long)T.z1 * P.aux_s1 + (long long)T.z2 * P.aux_s2;
+            const int rows = min(32, P.M - m_base);
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = half; c < BN / 32; c += 2) {
                 float v[32];
                 tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, v);
                 const int n0 = T.tn * BN + c * 32;
-                if (!row_ok || n0 >= P.N) continue;
+                if (rows <= 0 || n0 >= P.N) continue;  // warp-uniform
+                if (!P.staged) {  // bf16 output: each thread stores its row's 32 columns (64 B)
+                    const int m = m_base + lane;
+                    if (m >= P.M) continue;
+                    const long long c_off = zc + (long long)m * P.ldc;
                 const bool full_chunk = n0 + 32 <= P.N;
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] *= P.alpha;
@@ -332,58 +373,161 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                 }
                 if (P.epi & kEpiBias) {
+                    if (full_chunk && P.vec_bias) {  // same 64 B for every row: 4 x 16 B broadcast loads
+                        const uint4* b4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(P.bias) + n0);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (!full_chunk && n0 + j >= P.N) break;
-                        v[j] += P.bias_f32 ? static_cast<const float*>(P.bias)[n0 + j]
-                                           : bf16_bits_to_f32(static_cast<const uint16_t*>(P.bias)[n0 + j]);
+                        for (int w = 0; w < 4; ++w) add8(v, 8 * w, b4[w]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            if (!full_chunk && n0 + j >= P.N) continue;
+                            v[j] += P.bias_f32 ? static_cast<const float*>(P.bias)[n0 + j]
+                                               : bf16_bits_to_f32(static_cast<const uint16_t*>(P.bias)[n0 + j]);
+                        }
                     }
                 }
-                if (P.epi & kEpiAux) {
+                if (P.epi & kEpiGeluBwd) {
+                    const uint16_t* ap = P.aux + (long long)T.z1 * P.aux_s1 + (long long)T.z2 * P.aux_s2 +
+                                         (long long)m * P.ld_aux + n0;
+                    if (full_chunk && P.vec16_aux) {
+                        const uint4* a4 = reinterpret_cast<const uint4*>(ap);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) {
+                            const uint4 q4 = a4[w];
+                            const uint32_t u[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                            for (int e = 0; e < 8; ++e)
+                                v[8 * w + e] *= gelu_grad(bf16_bits_to_f32((e & 1) ? (u[e >> 1] >> 16) : (u[e >> 1] & 0xffffu)));
+                        }
+                    } else {
+                        for (int j = 0; j < 32; ++j)
+                            if (full_chunk || n0 + j < P.N) v[j] *= gelu_grad(bf16_bits_to_f32(ap[j]));
+                    }
+                }
+                if ((P.epi & kEpiAux) && !(P.epi & kEpiGeluBwd)) {
                     uint16_t* ap = P.aux + (long long)T.z1 * P.aux_s1 + (long long)T.z2 * P.aux_s2 +
                                    (long long)m * P.ld_aux + n0;
-                    if (full_chunk && P.vec_aux) {
+                    if (full_chunk && P.vec16_aux) {
                         uint4* a4 = reinterpret_cast<uint4*>(ap);
 #pragma unroll
                         for (int w = 0; w < 4; ++w)
                             a4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
                                                pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) ap[j] = (uint16_t)f32_to_bf16_bits(v[j]);
+                        #pragma unroll
+                        for (int j = 0; j < 32; ++j) if (n0 + j < P.N) ap[j] = (uint16_t)f32_to_bf16_bits(v[j]);
                     }
                 }
-                if (P.epi & kEpiGelu) {
+                if ((P.epi & kEpiGelu) && !(P.epi & kEpiGeluBwd)) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
                 }
                 if (P.epi & kEpiResidual) {
                     const uint16_t* rp = P.res + (long long)T.z1 * P.res_s1 + (long long)T.z2 * P.res_s2 +
                                          (long long)m * P.ld_res + n0;
+                    if (full_chunk && P.vec16_res) {
+                        const uint4* r4 = reinterpret_cast<const uint4*>(rp);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (full_chunk || n0 + j < P.N) v[j] += bf16_bits_to_f32(rp[j]);
+                        for (int w = 0; w < 4; ++w) add8(v, 8 * w, r4[w]);
+                    } else {
+                        for (int j = 0; j < 32; ++j)
+                            if (full_chunk || n0 + j < P.N) v[j] += bf16_bits_to_f32(rp[j]);
+                    }
                 }
                 if (P.c_f32) {
                     float* cp = static_cast<float*>(P.C) + c_off + n0;
-                    if (full_chunk && P.vec_c) {
+                    if (full_chunk && P.vec16_c) {
                         float4* c4 = reinterpret_cast<float4*>(cp);
 #pragma unroll
                         for (int w = 0; w < 8; ++w) c4[w] = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) cp[j] = v[j];
+                        #pragma unroll
+                        for (int j = 0; j < 32; ++j) if (n0 + j < P.N) cp[j] = v[j];
                     }
                 } else {
                     uint16_t* cp = static_cast<uint16_t*>(P.C) + c_off + n0;
-                    if (full_chunk && P.vec_c) {
+                    if (full_chunk && P.vec16_c) {
                         uint4* c4 = reinterpret_cast<uint4*>(cp);
 #pragma unroll
                         for (int w = 0; w < 4; ++w)
                             c4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
                                                pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
                     } else {
-                        for (int j = 0; j < 32 && n0 + j < P.N; ++j) cp[j] = (uint16_t)f32_to_bf16_bits(v[j]);
+                        #pragma unroll
+                        for (int j = 0; j < 32; ++j) if (n0 + j < P.N) cp[j] = (uint16_t)f32_to_bf16_bits(v[j]);
                     }
                 }
+                    continue;
+                }
+                float4* srow = reinterpret_cast<float4*>(stage + lane * 36);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) srow[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                __syncwarp();
+                const int n = n0 + sub * 4;
+                const int ncols = min(4, P.N - n);  // <= 0: lane idle
+                float bias[4] = {0.f, 0.f, 0.f, 0.f};
+                if ((P.epi & kEpiBias) && ncols > 0) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (k < ncols)
+                            bias[k] = P.bias_f32 ? static_cast<const float*>(P.bias)[n + k]
+                                                 : bf16_bits_to_f32(static_cast<const uint16_t*>(P.bias)[n + k]);
+                }
+                const bool vec = ncols == 4 && P.vec_c;
+#pragma unroll 2
+                for (int pass = 0; pass < 8; ++pass) {
+                    const int rr = pass * 4 + rsub;
+                    if (rr >= rows || ncols <= 0) continue;
+                    const long long m = m_base + rr;
+                    const float4 s4 = *reinterpret_cast<const float4*>(stage + rr * 36 + sub * 4);
+                    float x[4] = {s4.x * P.alpha, s4.y * P.alpha, s4.z * P.alpha, s4.w * P.alpha};
+                    const long long ci = zc + m * P.ldc + n;
+                    if (P.beta != 0.f) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k < ncols)
+                                x[k] += P.beta * (P.c_f32 ? static_cast<const float*>(P.C)[ci + k]
+                                                          : bf16_bits_to_f32(static_cast<const uint16_t*>(P.C)[ci + k]));
+                    }
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) x[k] += bias[k];
+                    if (P.epi & (kEpiGeluBwd | kEpiAux)) {
+                        uint16_t* ap = P.aux + za + m * P.ld_aux + n;
+                        if (P.epi & kEpiGeluBwd) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                if (k < ncols) x[k] *= gelu_grad(bf16_bits_to_f32(ap[k]));
+                        } else if (vec && P.vec_aux) {
+                            *reinterpret_cast<uint2*>(ap) = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
+                        } else {
+                            for (int k = 0; k < ncols; ++k) ap[k] = (uint16_t)f32_to_bf16_bits(x[k]);
+                        }
+                    }
+                    if ((P.epi & kEpiGelu) && !(P.epi & kEpiGeluBwd)) {
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) x[k] = gelu_tanh(x[k]);
+                    }
+                    if (P.epi & kEpiResidual) {
+                        const uint16_t* rp = P.res + zr + m * P.ld_res + n;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            if (k < ncols) x[k] += bf16_bits_to_f32(rp[k]);
+                    }
+                    if (P.c_f32) {
+                        float* cp = static_cast<float*>(P.C) + ci;
+                        if (vec)
+                            *reinterpret_cast<float4*>(cp) = make_float4(x[0], x[1], x[2], x[3]);
+                        else
+                            for (int k = 0; k < ncols; ++k) cp[k] = x[k];
+                    } else {
+                        uint16_t* cp = static_cast<uint16_t*>(P.C) + ci;
+                        if (vec)
+                            *reinterpret_cast<uint2*>(cp) = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
+                        else
+                            for (int k = 0; k < ncols; ++k) cp[k] = (uint16_t)f32_to_bf16_bits(x[k]);
+                    }
+                }
+                __syncwarp();
             }
             tc_fence_before();
             __syncwarp();
@@ -394,7 +538,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         }
     }
-
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -442,7 +585,7 @@ static bool make_map(CUtensorMap* map, const void* base, long long inner, long l
 
 template <int BN, int STAGES>
 static size_t smem_bytes() {
-    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16;
+    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem;
 }
 
 template <int BN, int STAGES>
@@ -557,11 +700,20 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     P.epi = g.epilogue;
     P.causal = g.causal;
     {
-        const long long ce = g.c_f32 ? 4 : 2, align = 16 / ce;
-        P.vec_c = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % align == 0 && g.c_s1 % align == 0 &&
+        const long long align = 4;  // 4-element vectors: 16 B fp32 / 8 B bf16
+        P.vec_c = (reinterpret_cast<uintptr_t>(g.C) % (g.c_f32 ? 16 : 8) == 0) && g.ldc % align == 0 && g.c_s1 % align == 0 &&
                   g.c_s2 % align == 0;
-        P.vec_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
-                    g.aux_s2 % 8 == 0;
+        P.vec_aux = (reinterpret_cast<uintptr_t>(g.aux) % 8 == 0) && g.ld_aux % 4 == 0 && g.aux_s1 % 4 == 0 &&
+                    g.aux_s2 % 4 == 0;
+        const long long e16 = g.c_f32 ? 4 : 8;
+        P.vec16_c = (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % e16 == 0 && g.c_s1 % e16 == 0 &&
+                    g.c_s2 % e16 == 0;
+        P.vec16_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
+                      g.aux_s2 % 8 == 0;
+        P.staged = 0;
+        P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
+        P.vec16_res = (reinterpret_cast<uintptr_t>(g.residual) % 16 == 0) && g.ld_res % 8 == 0 && g.res_s1 % 8 == 0 &&
+                      g.res_s2 % 8 == 0;
     }
 
     CUtensorMap ma, mb;

@@ -370,7 +370,7 @@ cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, con
     return launched(2);
 }
 
-int colsum_rows(int T) { return T >= 4096 ? 64 : (T >= 256 ? 16 : 1); }
+int colsum_rows(int T) { return T >= 4096 ? 256 : (T >= 256 ? 32 : 1); }
 
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st) {
     const int R = colsum_rows(T);
@@ -544,6 +544,94 @@ cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* of
                               const int* n_uniq, int T, float* dwte, int h, cudaStream_t st) {
     embed_bwd_tok_dev_kernel<<<T, 256, 0, st>>>(dx, uniq, offs, pos, n_uniq, dwte, h);
     return launched(1);
+}
+}  // namespace gpt
+}  // namespace ah
+
+// ---------------------------------------------------------------------------------------
+// LayerNorm backward, split for occupancy: (1) dx, one warp per row, (2) dgamma/dbeta as a
+// deterministic two-level column reduction over fixed row chunks.
+// ---------------------------------------------------------------------------------------
+namespace ah {
+namespace gpt {
+namespace {
+__global__ void ln_bwd_dx_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                                 const float* __restrict__ mean, const float* __restrict__ rstd,
+                                 const uint16_t* __restrict__ g, const uint16_t* dres, uint16_t* dx, int T, int h) {
+    const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const uint16_t* xr = x + (size_t)row * h;
+    const uint16_t* dyr = dy + (size_t)row * h;
+    const float mu = mean[row], rs = rstd[row];
+    float s1 = 0.f, s2 = 0.f;
+    for (int c = lane * 8; c < h; c += 256) {
+        float xf[8], df[8], gf[8];
+        unpack8(ldg16(xr + c), xf);
+        unpack8(ldg16(dyr + c), df);
+        unpack8(ldg16(g + c), gf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float dg = df[i] * gf[i];
+            s1 += dg;
+            s2 += dg * (xf[i] - mu) * rs;
+        }
+    }
+    s1 = warp_sum(s1) / h;
+    s2 = warp_sum(s2) / h;
+    for (int c = lane * 8; c < h; c += 256) {
+        float xf[8], df[8], gf[8], rf[8];
+        unpack8(ldg16(xr + c), xf);
+        unpack8(ldg16(dyr + c), df);
+        unpack8(ldg16(g + c), gf);
+        if (dres) unpack8(ldg16(dres + (size_t)row * h + c), rf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float d = rs * (df[i] * gf[i] - s1 - (xf[i] - mu) * rs * s2);
+            if (dres) d += rf[i];
+            xf[i] = d;
+        }
+        stg16(dx + (size_t)row * h + c, pack8(xf));
+    }
+}
+
+// part[r][c] = sum_{rows in chunk r} dy*xhat (c < h) ; part[r][h + c] = sum dy
+__global__ void ln_bwd_dgdb_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                                   const float* __restrict__ mean, const float* __restrict__ rstd, int T, int h,
+                                   int rows, float* __restrict__ part) {
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (c >= h) return;
+    const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+    float dg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, db[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int r = r0; r < r1; ++r) {
+        float xf[8], df[8];
+        unpack8(ldg16(x + (size_t)r * h + c), xf);
+        unpack8(ldg16(dy + (size_t)r * h + c), df);
+        const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            dg[i] += df[i] * (xf[i] - mu) * rs;
+            db[i] += df[i];
+        }
+    }
+    float* dst = part + (size_t)blockIdx.y * 2 * h;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        dst[c + i] = dg[i];
+        dst[h + c + i] = db[i];
+    }
+}
+}  // namespace
+
+int reduce_chunks(int T) { return T >= 4096 ? 256 : (T >= 512 ? 32 : 1); }
+
+cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
+                    const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st) {
+    ln_bwd_dx_kernel<<<(T + 7) / 8, 256, 0, st>>>(dy, x, mean, rstd, g, dres, dx, T, h);
+    const int R = reduce_chunks(T), rows = (T + R - 1) / R;
+    ln_bwd_dgdb_kernel<<<dim3((h / 8 + 127) / 128, R), 128, 0, st>>>(dy, x, mean, rstd, T, h, rows, part);
+    colsum_finish_kernel<<<(2 * h + 255) / 256, 256, 0, st>>>(part, R, 2 * h, dgdb, 0, nullptr);
+    return launched(3);
 }
 }  // namespace gpt
 }  // namespace ah

@@ -16,6 +16,11 @@ cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint
 int ln_bwd_ctas(int T);
 cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
                    const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st);
+// Split LayerNorm backward (dx kernel + deterministic dgamma/dbeta column reduction); same
+// contract as ln_bwd; part: >= reduce_chunks(T) * 2h floats.
+int reduce_chunks(int T);
+cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
+                    const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st);
 // Column sums of X[T][N] (row stride ldx) -> out[N] (bf16 or fp32); part: >= colsum_rows(T)*N floats.
 int colsum_rows(int T);
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);

@@ -496,7 +496,7 @@ void Trainer::head_forward_backward(Iter& it) {
     wg.A = logits_; wg.a_mn_major = 1; wg.lda = d_.Vp; wg.B = xf_; wg.b_mn_major = 1; wg.ldb = h;
     wg.C = dwte_; wg.c_f32 = 1; wg.ldc = h;
     check(gemm::run(wg, st), "head wgrad");
-    check(gpt::ln_bwd(ws_.dln, x_[(size_t)d_.L], meanf_, rstdf_, lnf_b_, nullptr, gx_[d_.L & 1], dlnf_b_, ws_.part,
+    check(gpt::ln_bwd2(ws_.dln, x_[(size_t)d_.L], meanf_, rstdf_, lnf_b_, nullptr, gx_[d_.L & 1], dlnf_b_, ws_.part,
                       T, h, st),
           "lnf bwd");
 }

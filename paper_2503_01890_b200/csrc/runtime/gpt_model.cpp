@@ -212,16 +212,21 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
     const float scale = 1.0f / std::sqrt((float)hd);
 
     // ---- MLP out: x_out = x2 + gelu Wfc2^T + b_fc2
-    AH_TRY(gemm::run(linear_dgrad(d, dy, h, W + o.w_fc2, 4 * h, ws.d4h), st));  // dgelu
+    {  // dfc_pre = (dy Wfc2) * GELU'(fc_pre): GELU backward fused into the dgrad epilogue
+        GemmArgs g = linear_dgrad(d, dy, h, W + o.w_fc2, 4 * h, ws.d4h);
+        g.epilogue = gemm::kEpiGeluBwd;
+        g.aux = a.fc_pre;
+        g.ld_aux = 4 * h;
+        AH_TRY(gemm::run(g, st));
+    }
     AH_TRY(gemm::run(linear_wgrad(d, dy, h, a.gelu, 4 * h, W + o.w_fc2), st));  // dWfc2 -> slot
     AH_TRY(gpt::colsum(dy, T, h, h, ws.part, W + o.b_fc2, 0, st));
-    AH_TRY(gpt::gelu_bwd(ws.d4h, a.fc_pre, ws.d4h, (size_t)T * 4 * h, st));     // dfc_pre
     // ---- MLP in: fc_pre = ln2 Wfc^T + b_fc
     AH_TRY(gemm::run(linear_dgrad(d, ws.d4h, 4 * h, W + o.w_fc, h, ws.dln), st));
     AH_TRY(gemm::run(linear_wgrad(d, ws.d4h, 4 * h, a.ln2, h, W + o.w_fc), st));
     AH_TRY(gpt::colsum(ws.d4h, T, 4 * h, 4 * h, ws.part, W + o.b_fc, 0, st));
     // ---- LN2 (+ residual path dy)
-    AH_TRY(gpt::ln_bwd(ws.dln, a.x2, a.mean2, a.rstd2, W + o.ln2_g, dy, ws.dx2, W + o.ln2_g, ws.part, T, h, st));
+    AH_TRY(gpt::ln_bwd2(ws.dln, a.x2, a.mean2, a.rstd2, W + o.ln2_g, dy, ws.dx2, W + o.ln2_g, ws.part, T, h, st));
     // ---- attention out-projection: x2 = x_in + att Wproj^T + b_proj
     AH_TRY(gemm::run(linear_dgrad(d, ws.dx2, h, W + o.w_proj, h, ws.datt), st));
     AH_TRY(gemm::run(linear_wgrad(d, ws.dx2, h, a.att, h, W + o.w_proj), st));
@@ -275,7 +280,7 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
     AH_TRY(gemm::run(linear_wgrad(d, ws.dqkv, 3 * h, a.ln1, h, W + o.w_qkv), st));
     AH_TRY(gpt::colsum(ws.dqkv, T, 3 * h, 3 * h, ws.part, W + o.b_qkv, 0, st));
     // ---- LN1 (+ residual path dx2)
-    AH_TRY(gpt::ln_bwd(ws.dln, x_in, a.mean1, a.rstd1, W + o.ln1_g, ws.dx2, dx, W + o.ln1_g, ws.part, T, h, st));
+    AH_TRY(gpt::ln_bwd2(ws.dln, x_in, a.mean1, a.rstd1, W + o.ln1_g, ws.dx2, dx, W + o.ln1_g, ws.part, T, h, st));
     return cudaSuccess;
 }
 

@@ -124,3 +124,27 @@ def test_gemm_causal_modes(cuda_device, native, mode):
             ref = P.float().transpose(-1, -2) @ V.float()
         torch.cuda.synchronize()
         assert rel_err(out, ref) < 2e-3
+
+
+def test_gemm_gelu_bwd_epilogue(cuda_device, native):
+    """dX = (dY W) * GELU'(pre) fused in the epilogue (the fc2 dgrad of the MLP backward)."""
+    import ctypes as C
+    from paper_2503_01890_b200 import _native as N
+    M, Nn, K = 512, 1024, 256
+    A, B, a_arg, b_arg = operands(M, Nn, K, 0, 1, seed=5)
+    pre = torch.randn(M, Nn, device="cuda").bfloat16()
+    out = torch.empty(M, Nn, device="cuda", dtype=torch.bfloat16)
+    d = N.GemmDesc()
+    d.M, d.N, d.K, d.batch1, d.batch2 = M, Nn, K, 1, 1
+    d.A, d.lda = a_arg.data_ptr(), K
+    d.B, d.b_mn_major, d.ldb = b_arg.data_ptr(), 1, Nn
+    d.C, d.ldc = out.data_ptr(), Nn
+    d.aux, d.ld_aux = pre.data_ptr(), Nn
+    d.alpha, d.epilogue = 1.0, 32
+    N.check(N.lib().ah_gemm_bf16(C.byref(d), torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    x = pre.float().requires_grad_(True)
+    y = torch.nn.functional.gelu(x, approximate="tanh")
+    g = A.float() @ B.float().T
+    y.backward(g)
+    assert rel_err(out, x.grad) < 1e-2
