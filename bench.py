@@ -228,6 +228,20 @@ def main():
     launches = N.lib().ah_kernel_launches() - L0
     torch.cuda.synchronize()
     loss = tr.drain()
+    st_t = tr.stats()  # offload-overlap window = the last timed iterations
+    wi = max(1.0, st_t["window_iters"])
+    copy_ms = st_t["h2d_busy_ms"] + st_t["d2h_busy_ms"]
+    offload = {
+        "hidden_frac": (1.0 - st_t["offload_blocked_ms"] / copy_ms) if copy_ms > 0 else None,
+        "compute_blocked_ms_per_step": st_t["offload_blocked_ms"] / wi,
+        "h2d_ms_per_step": st_t["h2d_busy_ms"] / wi, "d2h_ms_per_step": st_t["d2h_busy_ms"] / wi,
+        "compute_busy_ms_per_step": st_t["compute_busy_ms"] / wi,
+        "h2d_gbps": st_t["h2d_gbps"], "d2h_gbps": st_t["d2h_gbps"],
+        "pinned_copy_peak_gbps": [prof["h2d_bw"] / 1e9, prof["d2h_bw"] / 1e9],
+        "window_iters": st_t["window_iters"],
+        "definition": "hidden = 1 - (compute-stream idle time before ops that depend on a prefetch / "
+                      "offload / CPU-optimizer op) / (H2D + D2H busy time), CUDA-event timestamps",
+    }
     ms_t = torch.tensor([ms], device="cuda")
     if dist:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -277,6 +291,7 @@ def main():
                  "sim_steady_ms": st["sim_steady_s"] * 1e3,
                  "lane_busy_ms_per_step": [x / max(1, a.steps + ke + a.warmup) for x in st["lane_busy_ms"]],
                  "h2d_bytes_per_step": st["h2d_bytes"], "d2h_bytes_per_step": st["d2h_bytes"]},
+        "offload": offload,
         "profiled_rates": prof,
         "clocks": clocks.summary(),
     }

@@ -183,6 +183,11 @@ typedef struct ah_trainer_stats {
     int32_t lane_ops[4];
     int64_t h2d_bytes, d2h_bytes; /* parameter prefetch / grad offload bytes per iteration */
     int32_t kernels_per_iter;     /* our kernel launches per iteration */
+    /* Offload overlap over the last drained window (CUDA-event timestamps): compute-lane time
+     * spent waiting for a ParamPrefetch / GradOffload / CpuOptim dependency, and the busy time
+     * of the copy lanes. hidden = 1 - blocked / (h2d + d2h busy). */
+    double window_iters, compute_busy_ms, h2d_busy_ms, d2h_busy_ms, offload_blocked_ms;
+    double h2d_gbps, d2h_gbps; /* achieved host-link bandwidth of the copy ops */
 } ah_trainer_stats;
 
 int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);

@@ -142,6 +142,9 @@ class TrainerStats(C.Structure):
         ("pool_peak_bytes", C.c_int64), ("static_bytes", C.c_int64), ("sim_steady_s", C.c_double),
         ("lane_busy_ms", C.c_double * 4), ("lane_ops", C.c_int32 * 4),
         ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64), ("kernels_per_iter", C.c_int32),
+        ("window_iters", C.c_double), ("compute_busy_ms", C.c_double), ("h2d_busy_ms", C.c_double),
+        ("d2h_busy_ms", C.c_double), ("offload_blocked_ms", C.c_double), ("h2d_gbps", C.c_double),
+        ("d2h_gbps", C.c_double),
     ]
 
 

@@ -377,8 +377,8 @@ cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* 
     const int rows = (T + R - 1) / R;
     dim3 grid((N / 8 + 127) / 128, R);
     colsum_partial_kernel<<<grid, 128, 0, st>>>(X, T, N, ldx, rows, part);
-    colsum_finish_kernel<<<(N + 255) / 256, 256, 0, st>>>(part, R, N, out, out_f32, nullptr);
-    return launched(2);
+    launched(1);
+    return colsum_finish_wide(part, R, N, out, out_f32, st);
 }
 
 cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st) {
@@ -630,8 +630,8 @@ cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, co
     ln_bwd_dx_kernel<<<(T + 7) / 8, 256, 0, st>>>(dy, x, mean, rstd, g, dres, dx, T, h);
     const int R = reduce_chunks(T), rows = (T + R - 1) / R;
     ln_bwd_dgdb_kernel<<<dim3((h / 8 + 127) / 128, R), 128, 0, st>>>(dy, x, mean, rstd, T, h, rows, part);
-    colsum_finish_kernel<<<(2 * h + 255) / 256, 256, 0, st>>>(part, R, 2 * h, dgdb, 0, nullptr);
-    return launched(3);
+    launched(2);
+    return colsum_finish_wide(part, R, 2 * h, dgdb, 0, st);
 }
 }  // namespace gpt
 }  // namespace ah

@@ -26,6 +26,10 @@ int colsum_rows(int T);
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);
 cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);
+// Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.
+cudaError_t softmax_fwd2(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
+cudaError_t softmax_bwd2(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);
+cudaError_t colsum_finish_wide(const float* part, int R, int N, void* out, int out_f32, cudaStream_t st);
 cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre, size_t n, cudaStream_t st);
 cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
                           cudaStream_t st);

@@ -762,6 +762,7 @@ float Trainer::drain() {
                 o.host_ms = -1.0;  // counted
             }
     }
+    account_window();
     last_loss_ = *loss_host_;
     return last_loss_;
 }
@@ -819,6 +820,13 @@ void Trainer::stats(ah_trainer_stats* s) {
     const int64_t per_block = dp_ ? (int64_t)shard_ : profile_.block.m_p;  // host-link elements
     s->h2d_bytes = 2 * per_block * (strategy_.o_hat + std::max(0, strategy_.p_hat));
     s->d2h_bytes = 2 * per_block * strategy_.o_hat;
+    s->window_iters = win_iters_;
+    s->compute_busy_ms = win_compute_ms_;
+    s->h2d_busy_ms = win_h2d_ms_;
+    s->d2h_busy_ms = win_d2h_ms_;
+    s->offload_blocked_ms = win_blocked_ms_;
+    s->h2d_gbps = win_h2d_ms_ > 0 ? win_h2d_bytes_ / (win_h2d_ms_ * 1e6) : 0.0;
+    s->d2h_gbps = win_d2h_ms_ > 0 ? win_d2h_bytes_ / (win_d2h_ms_ * 1e6) : 0.0;
 }
 
 std::string Trainer::trace_json() {
@@ -964,6 +972,64 @@ float Trainer::timer(bool stop) {
     float ms = 0.f;
     check(cudaEventElapsedTime(&ms, timer_ev_[0], timer_ev_[1]), "elapsed");
     return ms;
+}
+
+}  // namespace ah
+
+namespace ah {
+
+// Offload overlap of the drained window: for every compute op that depends on a copy-lane or
+// CPU op, the idle gap before it on the compute stream (previous compute op end -> its start)
+// is time the compute lane was blocked by offloading.
+void Trainer::account_window() {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (iters_.empty()) return;
+    cudaEvent_t origin = nullptr;
+    for (auto& kv : iters_.front()->ops)
+        if (kv.second.kind == OpKind::Forward && kv.second.block == 1) origin = kv.second.t0;
+    if (!origin) return;
+    struct Span {
+        double a, b;
+        bool waits_offload;
+    };
+    std::vector<Span> comp;
+    double h2d = 0, d2h = 0, hb = 0, db = 0;
+    const double wbytes = 2.0 * (double)(dp_ ? shard_ : d_.m_p());
+    for (Iter* it : iters_)
+        for (auto& kv : it->ops) {
+            RtOp& o = kv.second;
+            if (o.lane == kCpu) continue;
+            float a = 0, b = 0;
+            if (cudaEventElapsedTime(&a, origin, o.t0) != cudaSuccess) continue;
+            if (cudaEventElapsedTime(&b, origin, o.t1) != cudaSuccess) continue;
+            if (o.lane == kCompute) {
+                bool w = false;
+                for (const auto& dp : o.deps) {
+                    const int k = dp.second.kind;
+                    w |= k == (int)OpKind::ParamPrefetch || k == (int)OpKind::GradOffload || k == (int)OpKind::CpuOptim;
+                }
+                comp.push_back({a, b, w});
+            } else if (o.lane == kH2D) {
+                h2d += b - a;
+                if (blocks_[(size_t)o.block].o) hb += wbytes;
+            } else {
+                d2h += b - a;
+                db += wbytes;
+            }
+        }
+    std::sort(comp.begin(), comp.end(), [](const Span& x, const Span& y) { return x.a < y.a; });
+    double busy = 0, blocked = 0;
+    for (size_t i = 0; i < comp.size(); ++i) {
+        busy += comp[i].b - comp[i].a;
+        if (i > 0 && comp[i].waits_offload) blocked += std::max(0.0, comp[i].a - comp[i - 1].b);
+    }
+    win_iters_ = (double)iters_.size();
+    win_compute_ms_ = busy;
+    win_h2d_ms_ = h2d;
+    win_d2h_ms_ = d2h;
+    win_blocked_ms_ = blocked;
+    win_h2d_bytes_ = hb;
+    win_d2h_bytes_ = db;
 }
 
 }  // namespace ah

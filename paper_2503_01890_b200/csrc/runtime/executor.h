@@ -179,6 +179,10 @@ private:
     size_t lane_pos_[4] = {0, 0, 0, 0};  // index into iters_ window per lane
     LaneStats lane_stats_[4];
     float last_loss_ = 0.f;
+    // offload-overlap accounting of the last drain (see ah_trainer_stats)
+    double win_iters_ = 0, win_compute_ms_ = 0, win_h2d_ms_ = 0, win_d2h_ms_ = 0, win_blocked_ms_ = 0;
+    double win_h2d_bytes_ = 0, win_d2h_bytes_ = 0;
+    void account_window();
 };
 
 }  // namespace ah

@@ -166,7 +166,7 @@ cudaError_t block_forward(const GptDims& d, const uint16_t* W, const uint16_t* x
         g.causal = gemm::kCausalSkipUpper;
         AH_TRY(gemm::run(g, st));
     }
-    AH_TRY(gpt::softmax_fwd(ws.S, a.P, (long long)d.B * d.nh * s, s, st));
+    AH_TRY(gpt::softmax_fwd2(ws.S, a.P, (long long)d.B * d.nh * s, s, st));
     {  // att[b, t, head*hd + j] = sum_k P[t][k] V[k][j]
         GemmArgs g;
         heads(g, d);
@@ -242,7 +242,7 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         g.causal = gemm::kCausalSkipUpper;
         AH_TRY(gemm::run(g, st));
     }
-    AH_TRY(gpt::softmax_bwd(a.P, ws.S, ws.dS, (long long)d.B * d.nh * s, s, st));
+    AH_TRY(gpt::softmax_bwd2(a.P, ws.S, ws.dS, (long long)d.B * d.nh * s, s, st));
     {  // dV = P^T dO
         GemmArgs g;
         heads(g, d);
