@@ -134,6 +134,13 @@ typedef struct ah_gemm_desc {
 
 int ah_gemm_bf16(const ah_gemm_desc* desc, void* stream);
 
+/* Fused causal attention forward of one block (part of OpKind::Forward / Recompute; the
+ * reference's 4*b*s^2*h attention term of t_fp, workload.cpp:63): qkv [B, s, 3h] bf16 ->
+ * O [B, s, h] bf16 and the normalised probabilities P [B, heads, s, s] bf16 (saved for the
+ * backward; zero above the diagonal within each 128-row tile). head_dim must be 128. */
+int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
+                     int32_t heads, int32_t head_dim, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Training executor: one GPT iteration = hetsim::build_iteration_ops(profile, strategy, k)
  * (proj/core/src/simulator.cpp:91-229) executed on B200 in the per-lane order of

@@ -26,6 +26,11 @@ int colsum_rows(int T);
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);
 cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);
+// Fused causal attention forward (attn_fwd.cu): qkv [B, s, 3h] -> O [B, s, h] and the
+// normalised probabilities P [B, nh, s, s] (bf16, zero above the diagonal up to the tile end).
+bool attn_fwd_supported(int hd, int s);
+cudaError_t attn_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int B, int s, int nh, int hd, float scale,
+                     cudaStream_t st);
 // Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.
 cudaError_t softmax_fwd2(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd2(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);

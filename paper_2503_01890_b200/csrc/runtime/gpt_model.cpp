@@ -4,6 +4,8 @@
 #include "gpt_model.h"
 
 #include <cmath>
+#include <cstdlib>
+#include <string>
 
 #include "../kernels/gemm.h"
 #include "../kernels/gpt_kernels.h"
@@ -68,6 +70,16 @@ GemmArgs linear_wgrad(const GptDims& d, const uint16_t* dY, int N, const uint16_
     g.C = dW;
     g.ldc = K;
     return g;
+}
+
+// Fused tcgen05 attention forward when the shape allows it (head_dim 128, s % 128 == 0);
+// AH_ATTENTION=unfused selects the GEMM + softmax + GEMM path (A/B checks, other shapes).
+bool fused_attention(const GptDims& d) {
+    static const bool off = [] {
+        const char* e = std::getenv("AH_ATTENTION");
+        return e && std::string(e) == "unfused";
+    }();
+    return !off && gpt::attn_fwd_supported(d.hd, d.s);
 }
 
 // Per-(head, sequence) view helpers: z1 = head, z2 = sequence.
@@ -155,6 +167,9 @@ cudaError_t block_forward(const GptDims& d, const uint16_t* W, const uint16_t* x
         g.bias = W + o.b_qkv;
         AH_TRY(gemm::run(g, st));
     }
+    if (fused_attention(d)) {  // one tcgen05 kernel: S, softmax, P (kept for the backward), P V
+        AH_TRY(gpt::attn_fwd(a.qkv, a.P, a.att, d.B, s, d.nh, hd, 1.0f / std::sqrt((float)hd), st));
+    } else {
     {  // S = Q K^T / sqrt(hd), causal tiles only, fp32
         GemmArgs g;
         heads(g, d);
@@ -177,6 +192,7 @@ cudaError_t block_forward(const GptDims& d, const uint16_t* W, const uint16_t* x
         g.causal = gemm::kCausalKUptoM;
         AH_TRY(gemm::run(g, st));
     }
+    }  // unfused attention
     {  // x2 = x_in + att Wproj^T + b
         GemmArgs g = linear_fwd(d, a.att, h, W + o.w_proj, h, a.x2);
         g.epilogue = gemm::kEpiBias | gemm::kEpiResidual;
