@@ -7,8 +7,9 @@
 // O accumulator never needs the online-softmax rescale. Compared with GEMM(S fp32) + softmax +
 // GEMM(P V) this removes the fp32 score round trip through HBM.
 //
-// Warp roles (256 threads): 0 TMA producer, 1 MMA issuer (single thread), 2 TMEM allocator,
-// 4-7 softmax / epilogue (thread = query row; warp w reads TMEM lanes 32*(w%4)...).
+// Warp roles (384 threads): 0 TMA producer, 1 MMA issuer (single thread), 2 TMEM allocator,
+// 4-11 softmax / epilogue (thread = query row, two warps per row quarter splitting the keys;
+// warp w reads TMEM lanes 32*(w%4)...).
 // TMEM: S double buffer (2 x 128 fp32 columns) + O (128 columns).
 // Shapes: head_dim = 128, seq_len % 128 == 0.
 #include <cuda.h>
@@ -28,7 +29,7 @@ using namespace ah::tc;
 
 constexpr int kHD = 128, kBQ = 128, kBK = 128;
 constexpr uint32_t kTile = kBQ * kHD * 2;  // 32 KB: one 128 x 128 bf16 operand tile
-constexpr int kThreads = 256;
+constexpr int kThreads = 384;  // + 8 softmax warps (4..11)
 
 struct AttnParams {
     int s, nh, B, h;
@@ -72,9 +73,9 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             mbar_init(smem_u32(&kv_full[i]), 1);
             mbar_init(smem_u32(&kv_empty[i]), 1);
             mbar_init(smem_u32(&s_full[i]), 1);
-            mbar_init(smem_u32(&s_free[i]), 4);
+            mbar_init(smem_u32(&s_free[i]), 8);
         }
-        mbar_init(smem_u32(p_full), 4);
+        mbar_init(smem_u32(p_full), 8);
         mbar_init(smem_u32(p_free), 1);
         mbar_init(smem_u32(o_full), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -156,26 +157,31 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             }
             commit(smem_u32(o_full));
         }
-    } else if (warp >= 4) {  // ===== softmax / epilogue: thread = query row =====
+    } else if (warp >= 4) {  // ===== softmax / epilogue: thread = query row, one half of the keys =====
+        // 8 warps: two per TMEM lane quarter, each owning 64 of a tile's 128 key columns, so
+        // each SM sub-partition runs two independent exp2 streams.
+        const int half = (warp - 4) >> 2;
         const int r = (warp & 3) * 32 + lane;
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         const int q = qt * kBQ + r;
+        float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [2 halves][2 (m, l)][128 rows]
         float m = -INFINITY, l = 0.f;
-        for (int j = 0; j < n; ++j) {  // pass 1: exact row max and sum
+        for (int j = 0; j < n; ++j) {  // pass 1: exact row max and sum over this half's keys
             const int buf = j & 1, u = j >> 1;
             mbar_wait(smem_u32(&s_full[buf]), u & 1);
             fence_after();
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 float v[32];
-                ld32(tmem + lane_base + buf * 128 + c * 32, v);
+                const int col0 = half * 64 + c * 32;
+                ld32(tmem + lane_base + buf * 128 + col0, v);
                 float cm = -INFINITY;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const int key = j * kBK + c * 32 + i;
-                    v[i] = key <= q ? v[i] * A.scale_log2 : -INFINITY;
+                    v[i] = j * kBK + col0 + i <= q ? v[i] * A.scale_log2 : -INFINITY;
                     cm = fmaxf(cm, v[i]);
                 }
+                if (cm == -INFINITY) continue;  // fully masked chunk
                 const float mn = fmaxf(m, cm);
                 float add = 0.f;
 #pragma unroll
@@ -187,6 +193,15 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&s_free[buf]));
         }
+        red[(half * 2 + 0) * 128 + r] = m;
+        red[(half * 2 + 1) * 128 + r] = l;
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the 8 softmax warps only
+        {
+            const float mo = red[((half ^ 1) * 2 + 0) * 128 + r], lo = red[((half ^ 1) * 2 + 1) * 128 + r];
+            const float mt = fmaxf(m, mo);
+            l = (m == -INFINITY ? 0.f : l * exp2f(m - mt)) + (mo == -INFINITY ? 0.f : lo * exp2f(mo - mt));
+            m = mt;
+        }
         const float inv_l = 1.f / l;
         uint16_t* prow = A.P + (((size_t)b * A.nh + head) * A.s + q) * (size_t)A.s;
         for (int j = 0; j < n; ++j) {  // pass 2: normalised P -> smem (A operand) + HBM
@@ -195,26 +210,26 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             fence_after();
             if (j > 0) mbar_wait(smem_u32(p_free), (j - 1) & 1);
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 2; ++c) {
                 float v[32];
-                ld32(tmem + lane_base + buf * 128 + c * 32, v);
+                const int col0 = half * 64 + c * 32;
+                ld32(tmem + lane_base + buf * 128 + col0, v);
                 uint32_t w[16];
 #pragma unroll
                 for (int i = 0; i < 16; ++i) {
-                    const int key = j * kBK + c * 32 + 2 * i;
+                    const int key = j * kBK + col0 + 2 * i;
                     const float p0 = key <= q ? exp2f(v[2 * i] * A.scale_log2 - m) * inv_l : 0.f;
                     const float p1 = key + 1 <= q ? exp2f(v[2 * i + 1] * A.scale_log2 - m) * inv_l : 0.f;
                     w[i] = pack_bf16x2(p0, p1);
                 }
-                // smem: K-major SWIZZLE_128B tile, key columns c*32 .. c*32+31 of row r
-                const int atom = c >> 1;                  // keys 0-63 | 64-127
-                uint8_t* rowp = sP + atom * (kTile / 2) + r * 128;
+                // smem: K-major SWIZZLE_128B tile; this half's 64 keys are atom `half`
+                uint8_t* rowp = sP + half * (kTile / 2) + r * 128;
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8) {
-                    const int chunk = ((c & 1) * 4 + k8) ^ (r & 7);
+                    const int chunk = (c * 4 + k8) ^ (r & 7);
                     *reinterpret_cast<uint4*>(rowp + chunk * 16) = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
                 }
-                uint4* gp = reinterpret_cast<uint4*>(prow + j * kBK + c * 32);
+                uint4* gp = reinterpret_cast<uint4*>(prow + j * kBK + col0);
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8) gp[k8] = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
             }
@@ -230,10 +245,11 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         fence_after();
         uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
             float v[32];
-            ld32(tmem + lane_base + 256 + c * 32, v);
-            uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
+            const int col0 = half * 64 + c * 32;
+            ld32(tmem + lane_base + 256 + col0, v);
+            uint4* op = reinterpret_cast<uint4*>(orow + col0);
 #pragma unroll
             for (int k8 = 0; k8 < 4; ++k8)
                 op[k8] = make_uint4(pack_bf16x2(v[8 * k8], v[8 * k8 + 1]), pack_bf16x2(v[8 * k8 + 2], v[8 * k8 + 3]),
@@ -298,7 +314,7 @@ cudaError_t attn_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int B, int s
     a.scale_log2 = scale * 1.4426950408889634f;
     a.P = P;
     a.O = O;
-    const size_t smem = 1024 + 6 * (size_t)kTile + 16 * 8;
+    const size_t smem = 1024 + 6 * (size_t)kTile + 16 * 8 + 4 * 128 * 4;
     static bool cfg = false;
     if (!cfg) {
         cudaError_t e = cudaFuncSetAttribute(attn_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
