@@ -31,6 +31,11 @@ cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long l
 bool attn_fwd_supported(int hd, int s);
 cudaError_t attn_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int B, int s, int nh, int hd, float scale,
                      cudaStream_t st);
+// Fused causal attention backward (attn_bwd.cu): from qkv, O (= att), dO, P -> dS [B, nh, s, s]
+// (for the dQ GEMM) and dK (x scale), dV written into dqkv [B, s, 3h]; D: B*nh*s floats scratch.
+bool attn_bwd_supported(int hd, int s);
+cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const uint16_t* P, float* D,
+                     uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
 // Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.
 cudaError_t softmax_fwd2(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd2(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);

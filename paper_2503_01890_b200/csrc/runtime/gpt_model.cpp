@@ -248,6 +248,10 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
     AH_TRY(gemm::run(linear_wgrad(d, ws.dx2, h, a.att, h, W + o.w_proj), st));
     AH_TRY(gpt::colsum(ws.dx2, T, h, h, ws.part, W + o.b_proj, 0, st));
     // ---- attention core, per (head, sequence)
+    const bool fused = fused_attention(d);
+    if (fused) {  // one tcgen05 kernel: dP, dS (-> HBM for dQ), dV, dK; D = rowsum(dO * O) in ws.S
+        AH_TRY(gpt::attn_bwd(a.qkv, a.att, ws.datt, a.P, ws.S, ws.dS, ws.dqkv, d.B, s, d.nh, hd, scale, st));
+    } else {
     {  // dP = dO V^T (fp32, lower tiles)
         GemmArgs g;
         heads(g, d);
@@ -269,6 +273,7 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         g.causal = gemm::kCausalKFromM;
         AH_TRY(gemm::run(g, st));
     }
+    }  // unfused dP / softmax backward / dV
     {  // dQ = dS K * scale
         GemmArgs g;
         heads(g, d);
@@ -280,7 +285,7 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         g.causal = gemm::kCausalKUptoM;
         AH_TRY(gemm::run(g, st));
     }
-    {  // dK = dS^T Q * scale
+    if (!fused) {  // dK = dS^T Q * scale
         GemmArgs g;
         heads(g, d);
         g.M = s; g.N = hd; g.K = s;
