@@ -26,7 +26,9 @@
 
 #include <cstdio>
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -171,13 +173,10 @@ struct Tile {
     bool skip;
 };
 
-__device__ __forceinline__ Tile decode(const Params& P, int t, int BN) {
+__device__ __forceinline__ Tile decode_at(const Params& P, int z, int tm, int tn, int BN) {
     Tile T;
-    const int per_z = P.tiles_m * P.tiles_n;
-    const int z = t / per_z;
-    const int rem = t - z * per_z;
-    T.tm = rem / P.tiles_n;
-    T.tn = rem - T.tm * P.tiles_n;
+    T.tm = tm;
+    T.tn = tn;
     T.z1 = z % P.batch1;
     T.z2 = z / P.batch1;
     T.kb0 = 0;
@@ -196,7 +195,43 @@ __device__ __forceinline__ Tile decode(const Params& P, int t, int BN) {
     return T;
 }
 
-template <int BN, int STAGES>
+// Cluster tile ct -> this CTA's tile. A cluster of CS CTAs shares one B tile (same tn, z) and
+// takes CS consecutive M tiles; a rank past the last M tile computes an all-zero phantom tile
+// (TMA zero-fills, the epilogue masks rows >= M) so every CTA of a cluster runs the same
+// pipeline.
+template <int CS>
+__device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int crank) {
+    const int tmg = (P.tiles_m + CS - 1) / CS;
+    const int per_z = tmg * P.tiles_n;
+    const int z = ct / per_z;
+    const int rem = ct - z * per_z;
+    const int g = rem / P.tiles_n;
+    return decode_at(P, z, g * CS + crank, rem - g * P.tiles_n, BN);
+}
+
+__device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                               int c2, int c3, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"(mask)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+template <int BN, int STAGES, int CS>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params P) {
     constexpr uint32_t A_BYTES = BM * BK * 2;
@@ -216,13 +251,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const int crank = CS > 1 ? (int)cluster_rank() : 0;
 
     if (warp == 0 && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), 1);
+            mbar_init(smem_u32(&empty[s]), CS);  // one MMA commit per cluster CTA
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull[a]), 1);
@@ -237,7 +273,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
-    __syncthreads();
+    if (CS > 1)
+        cluster_sync_all();  // peers' barriers initialised before any multicast lands
+    else
+        __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
@@ -246,8 +285,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             // ===== TMA producer =====
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-                const Tile T = decode(P, t, BN);
+            for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
+                const Tile T = decode<CS>(P, ct, BN, crank);
                 if (T.skip) continue;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -263,12 +302,27 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int j = 0; j < BM / 64; ++j)
                             tma_load_4d(a_dst + j * (64 * BK * 2), &tmA, fb, T.tm * BM + j * 64, k0, T.z1, T.z2);
                     }
-                    if (!P.b_mn) {
-                        tma_load_4d(b_dst, &tmB, fb, k0, T.tn * BN, T.z1, T.z2);
-                    } else {
+                    if (CS == 1) {
+                        if (!P.b_mn) {
+                            tma_load_4d(b_dst, &tmB, fb, k0, T.tn * BN, T.z1, T.z2);
+                        } else {
 #pragma unroll
-                        for (int j = 0; j < BN / 64; ++j)
-                            tma_load_4d(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2);
+                            for (int j = 0; j < BN / 64; ++j)
+                                tma_load_4d(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2);
+                        }
+                    } else {  // this rank's 1/CS of the shared B tile, multicast to the cluster
+                        constexpr uint16_t mask = (1u << CS) - 1;
+                        if (!P.b_mn) {
+                            tma_load_4d_mc(b_dst + crank * (BN / CS) * 128, &tmB, fb, k0, T.tn * BN + crank * (BN / CS),
+                                           T.z1, T.z2, mask);
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < BN / 64 / CS; ++jj) {
+                                const int j = crank * (BN / 64 / CS) + jj;
+                                tma_load_4d_mc(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2,
+                                               mask);
+                            }
+                        }
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -291,8 +345,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-                const Tile T = decode(P, t, BN);
+            for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
+                const Tile T = decode<CS>(P, ct, BN, crank);
                 if (T.skip) continue;
                 mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
                 tc_fence_after();
@@ -308,7 +362,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         const uint64_t bd = smem_desc(b_addr + k * b_kstep, b_lbo, b_sbo);
                         tc_mma(d_tmem, ad, bd, idesc, (kb > T.kb0 || k > 0) ? 1u : 0u);
                     }
-                    tc_commit(smem_u32(&empty[stage]));
+                    if (CS == 1)
+                        tc_commit(smem_u32(&empty[stage]));
+                    else  // the stage holds peers' B slices: free it in every cluster CTA
+                        tc_commit_mc(smem_u32(&empty[stage]), (uint16_t)((1u << CS) - 1));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -336,8 +393,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         const int sub = lane & 7, rsub = lane >> 3;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-            const Tile T = decode(P, t, BN);
+        for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
+            const Tile T = decode<CS>(P, ct, BN, crank);
             if (T.skip) continue;
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
@@ -538,7 +595,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         }
     }
-    __syncthreads();
+    if (CS > 1)
+        cluster_sync_all();  // no peer may still multicast into / arrive on this CTA
+    else
+        __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
@@ -588,18 +648,35 @@ static size_t smem_bytes() {
     return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CS>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const Params& P, int grid,
                               cudaStream_t stream) {
     const size_t sm = smem_bytes<BN, STAGES>();
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, STAGES, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    gemm_kernel<BN, STAGES><<<grid, kThreads, sm, stream>>>(a, b, P);
-    return launched(1);
+    if (CS == 1) {
+        gemm_kernel<BN, STAGES, CS><<<grid, kThreads, sm, stream>>>(a, b, P);
+        return launched(1);
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES, CS>, a, b, P);
+    launched(1);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 struct TimingState {
@@ -716,16 +793,26 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
                       g.res_s2 % 8 == 0;
     }
 
+    // Clusters of 2 CTAs share (multicast) the B tile of two adjacent M tiles: every SM then
+    // pulls 16 KB instead of 32 KB of B per stage from L2 (the linear-layer GEMMs are L2-bound
+    // at one CTA per tile). Causal tiles have per-tile K ranges, so they stay unclustered.
+    static const bool no_cluster = [] {
+        const char* e = std::getenv("AH_GEMM_CLUSTER");
+        return e && std::string(e) == "1";
+    }();
+    const int CS = (!no_cluster && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
+    if (CS > 1) P.num_tiles = ((P.tiles_m + CS - 1) / CS) * P.tiles_n * P.batch1 * P.batch2;
     CUtensorMap ma, mb;
     const bool ok_a = g.a_mn_major
                           ? make_map(&ma, g.A, g.M, g.K, g.lda, P.batch1, g.a_s1, P.batch2, g.a_s2, 64, 64)
                           : make_map(&ma, g.A, g.K, g.M, g.lda, P.batch1, g.a_s1, P.batch2, g.a_s2, 64, BM);
     const bool ok_b = g.b_mn_major
                           ? make_map(&mb, g.B, g.N, g.K, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, 64)
-                          : make_map(&mb, g.B, g.K, g.N, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, BN);
+                          : make_map(&mb, g.B, g.K, g.N, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, BN / CS);
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
-    int grid = P.num_tiles < kNumSMs ? P.num_tiles : kNumSMs;
-    if (max_ctas > 0 && grid > max_ctas) grid = max_ctas;
+    const int max_clusters = kNumSMs / CS;
+    int grid = (P.num_tiles < max_clusters ? P.num_tiles : max_clusters) * CS;
+    if (max_ctas > 0 && grid > max_ctas) grid = (max_ctas / CS) * CS;
     cudaEvent_t ta = nullptr, tb = nullptr;
     bool timed = false;
     {
@@ -739,11 +826,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     }
     cudaError_t e;
     if (BN == 256)
-        e = launch_cfg<256, 4>(ma, mb, P, grid, stream);
+        e = CS == 2 ? launch_cfg<256, 4, 2>(ma, mb, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, P, grid, stream);
     else if (BN == 128)
-        e = launch_cfg<128, 6>(ma, mb, P, grid, stream);
+        e = launch_cfg<128, 6, 1>(ma, mb, P, grid, stream);
     else
-        e = launch_cfg<64, 8>(ma, mb, P, grid, stream);
+        e = launch_cfg<64, 8, 1>(ma, mb, P, grid, stream);
     if (timed) {
         cudaEventRecord(tb, stream);
         std::lock_guard<std::mutex> lk(timing().mu);
