@@ -101,6 +101,52 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def gemm_traffic():
+    """DRAM bytes (read + write) of one representative GEMM launch from the committed
+    `ncu --set full` capture (profiles/r1/gemm_fc_ncu.json: the 8192x8192x2048 MLP GEMM),
+    next to its algorithmic bytes (A + B + C once)."""
+    p = os.path.join(ROOT, "profiles", "r1", "gemm_fc_ncu.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return {"bytes": (d["dram_read"][0] + d["dram_write"][0]) * 1e6, "algorithmic_bytes": d["algorithmic_bytes_MB"] * 1e6,
+            "launch": d["shape"], "tensor_pipe_active_pct": d["tensor_pipe_active_pct_elapsed"][0],
+            "source": "profiles/r1/gemm_fc_ncu.json"}
+
+
+def adam_hbm(hbm_peak, sizes=(10_000_000, 100_000_000, 1_000_000_000), iters=10):
+    """Config C5: fused sm_100a AdamW, 28 algorithmic bytes/param (fp32 p/m/v
+    read+write, bf16 grad read, bf16 param write), CUDA events on the launching stream,
+    working set >> L2 at 100M+ params. Returns the sweep and the roofline at the largest size."""
+    import torch
+    from paper_2503_01890_b200 import optim
+    rows = []
+    for n in sizes:
+        p = torch.empty(n, device="cuda").normal_(0, 0.02)
+        m = torch.empty(n, device="cuda").normal_(0, 1e-3)
+        v = torch.empty(n, device="cuda").normal_(0, 1e-3) ** 2
+        g = torch.empty(n, device="cuda").normal_(0, 1e-2).bfloat16()
+        out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        hp = optim.hparams(step=10)
+        for _ in range(3):
+            optim.adam_step(p, m, v, g, out, hp=hp)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            optim.adam_step(p, m, v, g, out, hp=hp)
+        e1.record()
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / iters
+        rows.append({"params": n, "us": t * 1e6, "params_per_s": n / t, "GBps": 28 * n / t / 1e9})
+        del p, m, v, g, out
+        torch.cuda.empty_cache()
+    top = rows[-1]["GBps"]
+    return {"sweep": rows, "roofline": {"bound": "hbm", "achieved": top, "peak": hbm_peak, "unit": "GB/s",
+                                        "frac": top / hbm_peak, "bytes_per_param": 28,
+                                        "traffic": "28.0 B/param (ncu dram read+write, profiles/r1/SUMMARY.md)"}}
+
+
 def ref_cpu_path(m, budget, cpu_budget, rates, sample, threads, reps=3):
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_cpu_path")
     if not os.path.exists(exe):
@@ -264,6 +310,8 @@ def main():
     e2e = T * ke * world / (float(me_t.item()) / 1e3)
     st = tr.stats()
     tr.close()
+    torch.cuda.empty_cache()
+    adam = adam_hbm(peaks()[1])
 
     bf16_peak, hbm_peak, peak_kind = peaks()
     gemm_tflops = g_fl.value / (g_ms.value / 1e3) / 1e12 if g_ms.value > 0 else None
@@ -280,7 +328,8 @@ def main():
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * 4, "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_peak, "unit": "TFLOP/s",
-                     "frac": (gemm_tflops / bf16_peak) if gemm_tflops else None, "traffic": None,
+                     "frac": (gemm_tflops / bf16_peak) if gemm_tflops else None,
+                     "traffic": gemm_traffic(),
                      "kernel": "gemm_kernel (tcgen05)", "peak_kind": f"{peak_kind} sustained bf16",
                      "gemm_share_of_step": g_ms.value / ms if ms > 0 else None, "gemm_launches": int(g_n.value)},
         "model_flops_per_token": flops_per_token(m),
@@ -294,6 +343,7 @@ def main():
                  "lane_busy_ms_per_step": [x / max(1, a.steps + ke + a.warmup) for x in st["lane_busy_ms"]],
                  "h2d_bytes_per_step": st["h2d_bytes"], "d2h_bytes_per_step": st["d2h_bytes"]},
         "offload": offload,
+        "adam": adam,
         "profiled_rates": prof,
         "clocks": clocks.summary(),
     }
