@@ -213,6 +213,11 @@ int ah_trainer_schedule(void* trainer, char* buf, size_t cap);
  * -2 = final LayerNorm; n = element count written to out (host). */
 int ah_trainer_read_master(void* trainer, int32_t block, float* out, size_t n);
 int64_t ah_trainer_master_size(void* trainer, int32_t block);
+/* Optimizer-state checkpoint (fp32 master / m / v of every block and of the embedding state,
+ * plus the step counter), independent of the plan: load under a different (c, p, o) works.
+ * Load only into a freshly created trainer with the same model shape and dp layout. */
+int ah_trainer_save(void* trainer, const char* path);
+int ah_trainer_load(void* trainer, const char* path);
 int ah_trainer_trace(void* trainer, char* buf, size_t cap); /* Chrome trace JSON, measured */
 /* Device-timed region on the executor's compute stream: stop=0 drains then records the
  * start event; stop=1 drains all lanes, records the stop event and returns elapsed ms. */

@@ -194,3 +194,9 @@ def dp_shard(n: int, rank: int, size: int) -> tuple[int, int, int]:
     off, ln, sh = C.c_int64(), C.c_int64(), C.c_int64()
     check(lib().ah_dp_shard(n, rank, size, C.byref(off), C.byref(ln), C.byref(sh)), "ah_dp_shard")
     return off.value, ln.value, sh.value
+
+_EXTRA_SIGS.update({
+    "ah_trainer_save": ([C.c_void_p, C.c_char_p], C.c_int),
+    "ah_trainer_load": ([C.c_void_p, C.c_char_p], C.c_int),
+    "ah_attention_fwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
+})

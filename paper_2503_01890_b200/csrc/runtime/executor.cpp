@@ -211,6 +211,10 @@ void Trainer::allocate_and_init() {
     check(cudaDeviceGetDefaultMemPool(&pool_, 0), "mempool");
     uint64_t thr = UINT64_MAX;
     check(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
+    if (const char* e = std::getenv("AH_POOL_INTERNAL_DEPS")) {  // experiment knob: 0 = never make a
+        int on = std::atoi(e);                                     // stream wait on another lane's free
+        check(cudaMemPoolSetAttribute(pool_, cudaMemPoolReuseAllowInternalDependencies, &on), "mempool attr");
+    }
     size_t stat = 0;
     auto dalloc = [&](void** p, size_t bytes) {
         check(cudaMalloc(p, bytes), "cudaMalloc");
@@ -520,7 +524,7 @@ void Trainer::embed_backward_and_update(Iter& it) {
     }
     check(gpt::f32_to_bf16(dwte_, dwte_b_, nwte, st), "cvt");
     check(gpt::f32_to_bf16(dwpe_, dwpe_b_, nwpe, st), "cvt");
-    const int step = (int)it.k;
+    const int step = (step_base_ + (int)it.k);
     const float inv = 1.f / (float)dp_size_;
     AdamArgs a1 = adam_args(adam_, step, wte_, wte_m_, wte_v_, dwte_b_, wte_b_, nwte);
     AdamArgs a2 = adam_args(adam_, step, wpe_, wpe_m_, wpe_v_, dwpe_b_, wpe_b_, nwpe);
@@ -593,8 +597,8 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             break;
         }
         case OpKind::GpuOptim: {
-            AdamArgs aa = dp_ ? adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf + off, nullptr, shard_)
-                              : adam_args(adam_, (int)it.k, b.master, b.m1, b.m2, b.wbuf, nullptr, mp);
+            AdamArgs aa = dp_ ? adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf + off, nullptr, shard_)
+                              : adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf, nullptr, mp);
             aa.inv_scale = 1.f / (float)dp_size_;
             check(launch_adam(aa, st), "adam");
             free_wbuf();
@@ -635,7 +639,7 @@ void Trainer::run_d2h(Iter& it, RtOp& op) {
 void Trainer::run_cpu(Iter& it, RtOp& op) {
     BlockState& b = blocks_[(size_t)op.block];
     ah_adam_hparams hp = adam_;
-    hp.step = (int)it.k;
+    hp.step = (step_base_ + (int)it.k);
     const auto t0 = Clock::now();
     const size_t n = dp_ ? shard_ : d_.m_p();
     cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);

@@ -57,9 +57,16 @@ public:
     std::string trace_json();
     // drain + record start (stop=false) / drain + record stop and return elapsed ms (stop=true)
     float timer(bool stop);
+    // Optimizer-state checkpoint (fp32 master, m, v of this rank's part of every block + the
+    // replicated embedding state + the step counter). Plan-independent: a checkpoint taken
+    // under one (c, p, o) plan loads under another (GPU- or host-resident state alike).
+    void save(const std::string& path);
+    void load(const std::string& path);
 
 private:
     cudaEvent_t timer_ev_[2] = {nullptr, nullptr};
+    int step_base_ = 0;  // optimizer steps completed before this trainer (checkpoint resume)
+    friend struct CheckpointIO;
     // data parallel
     int dp_rank_ = 0, dp_size_ = 1;
     bool dp_ = false;      // collectives on

@@ -149,6 +149,14 @@ class Trainer:
         N.check(N.lib().ah_trainer_read_master(self._h, block, out.ctypes.data, n), "ah_trainer_read_master")
         return out
 
+    def save(self, path: str) -> None:
+        """Optimizer-state checkpoint (plan-independent)."""
+        N.check(N.lib().ah_trainer_save(self._h, path.encode()), "ah_trainer_save")
+
+    def load(self, path: str) -> None:
+        """Resume from save() into a fresh trainer (any plan, same model / dp layout)."""
+        N.check(N.lib().ah_trainer_load(self._h, path.encode()), "ah_trainer_load")
+
     def timer(self, stop: bool) -> float:
         ms = C.c_float()
         N.check(N.lib().ah_trainer_timer(self._h, int(stop), C.byref(ms)), "ah_trainer_timer")

@@ -121,3 +121,26 @@ def test_dp_collective_path_is_exact_on_one_rank(cuda_device, native):
         for a, b in zip(state, base_state):
             n = min(a.size, b.size)  # DP shard is padded to a multiple of 8
             assert np.array_equal(a[:n].view(np.uint32), b[:n].view(np.uint32)), plan
+
+
+def test_checkpoint_resume_across_plans(cuda_device, native, tmp_path):
+    """3 uninterrupted steps == 2 steps under one plan + save + load under another plan + 1 step
+    (bit-identical fp32 state and loss)."""
+    ref_loss, ref_state, _ = run_plan(PLANS[0], steps=3)
+    from paper_2503_01890_b200.trainer import PlanConfig
+    tr = make(plan=PlanConfig(fine_tune=False, gpu_mem_budget=1 << 40, **PLANS[4]))
+    for k in range(2):
+        tr.submit(*batch(k))
+    tr.drain()
+    path = str(tmp_path / "ck.bin")
+    tr.save(path)
+    tr.close()
+    tr = make(plan=PlanConfig(fine_tune=False, gpu_mem_budget=1 << 40, **PLANS[2]))
+    tr.load(path)
+    tr.submit(*batch(2))
+    loss = tr.drain()
+    state = [tr.master(i).copy() for i in range(-2, MODEL["num_blocks"] + 1)]
+    tr.close()
+    assert loss == ref_loss[-1]
+    for a, b in zip(state, ref_state):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
