@@ -27,6 +27,7 @@
 #include <cstdio>
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -40,8 +41,11 @@ namespace gemm {
 
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int kThreads = 384;  // warps 0-3: TMA / MMA / TMEM alloc / spare; 4-11: epilogue
-constexpr int kEpiWarps = 8;
+constexpr int kThreads = 384;
+constexpr int kEpiWarps = 8;  // warps 0-7: epilogue (two per TMEM lane quarter)
+// The single-thread producer / MMA roles take the highest warp ids (the sub-partition arbiter
+// issues highest-warp-id first), so epilogue ALU work cannot starve an MMA or TMA issue slot.
+constexpr int kWarpTMA = 8, kWarpMMA = 9, kWarpAlloc = 10;
 // The smem-transposed (staged) epilogue is compiled but disabled: with 8 epilogue warps its
 // staging slabs do not fit beside a 4-stage BN=256 ring. Direct row stores are used.
 constexpr int kStagedSmem = 0;
@@ -67,6 +71,8 @@ struct Params {
     int vec16_c, vec16_aux;  // 16-byte rows (direct path)
     int staged;              // smem-transposed epilogue (fp32 outputs)
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
+    int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE=1: skip the epilogue (profiling only)
+    int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
 };
 
 // ---------------------------------------------------------------------------------------
@@ -233,7 +239,8 @@ __device__ __forceinline__ void cluster_sync_all() {
 
 template <int BN, int STAGES, int CS>
 __global__ void __launch_bounds__(kThreads, 1)
-gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params P) {
+gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+            const __grid_constant__ CUtensorMap tmC, const Params P) {
     constexpr uint32_t A_BYTES = BM * BK * 2;
     constexpr uint32_t B_BYTES = BN * BK * 2;
     constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
@@ -248,12 +255,14 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint64_t* tfull = bars + 2 * STAGES;
     uint64_t* tempty = bars + 2 * STAGES + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 4);
+    // TMA-store staging: per epilogue warp two 32x32 bf16 slabs (SWIZZLE_64B), 1 KB past the barriers
+    uint8_t* cstage = reinterpret_cast<uint8_t*>(bars) + 1024;
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const int crank = CS > 1 ? (int)cluster_rank() : 0;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == kWarpTMA && lane == 0) {
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
         for (int s = 0; s < STAGES; ++s) {
@@ -267,7 +276,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    if (warp == 2) {
+    if (warp == kWarpAlloc) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
                      "r"(2 * BN));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -280,7 +289,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
 
-    if (warp == 0) {
+    if (warp == kWarpTMA) {
         if (lane == 0) {
             // ===== TMA producer =====
             int stage = 0;
@@ -331,7 +340,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == kWarpMMA) {
         if (lane == 0) {
             // ===== MMA issuer =====
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(P.a_mn) << 15) |
@@ -378,7 +387,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
             }
         }
-    } else if (warp >= 4) {
+    } else if (warp < kEpiWarps) {
         // ===== epilogue =====
         // TMEM -> registers (thread = row, 32 columns) -> per-warp smem slab -> each lane
         // re-reads 4 consecutive columns of a row, so a warp instruction covers 4 rows x 32
@@ -388,9 +397,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // epilogue warps per SM sub-partition, so the per-element work has the ILP to hide
         // under the next tile's MMAs
         const int q = warp & 3;  // TMEM lane quarter = 32-row slab of the tile
-        const int half = (warp - 4) >> 2;
-        float* stage = reinterpret_cast<float*>(tmem_holder + 4) + (warp - 4) * 32 * 36;
+        const int half = warp >> 2;
+        float* stage = reinterpret_cast<float*>(tmem_holder + 4) + warp * 32 * 36;
         const int sub = lane & 7, rsub = lane >> 3;
+        int epi_chunk = 0;  // TMA-store slabs used by this warp (double-buffered)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
@@ -409,11 +419,17 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, v);
                 const int n0 = T.tn * BN + c * 32;
                 if (rows <= 0 || n0 >= P.N) continue;  // warp-uniform
-                if (!P.staged) {  // bf16 output: each thread stores its row's 32 columns (64 B)
+                if (P.dbg_no_store) continue;  // diagnostics: main loop only
+                if (!P.staged) {  // bf16 output: each thread owns its row's 32 columns
                     const int m = m_base + lane;
-                    if (m >= P.M) continue;
+                    const bool row_live = m < P.M;
+                    if (!row_live && !P.tma_c) continue;
                     const long long c_off = zc + (long long)m * P.ldc;
                 const bool full_chunk = n0 + 32 <= P.N;
+                if (!row_live) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = 0.f;
+                } else {
 #pragma unroll
                 for (int j = 0; j < 32; ++j) v[j] *= P.alpha;
                 if (P.beta != 0.f) {
@@ -490,6 +506,31 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int j = 0; j < 32; ++j)
                             if (full_chunk || n0 + j < P.N) v[j] += bf16_bits_to_f32(rp[j]);
                     }
+                }
+                }  // row_live
+                if (P.tma_c) {  // registers -> swizzled smem slab -> one TMA bulk store per chunk
+                    uint8_t* slab = cstage + (warp * 2 + (epi_chunk & 1)) * 2048;
+                    if (epi_chunk >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int w = 0; w < 4; ++w) {
+                        const int chunk = w ^ ((lane >> 1) & 3);
+                        *reinterpret_cast<uint4*>(slab + lane * 64 + chunk * 16) =
+                            make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
+                                       pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tmC)),
+                            "r"(smem_u32(slab)), "r"(n0), "r"(m_base), "r"(T.z1), "r"(T.z2)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++epi_chunk;
+                    continue;
                 }
                 if (P.c_f32) {
                     float* cp = static_cast<float*>(P.C) + c_off + n0;
@@ -594,12 +635,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 acc_phase ^= 1;
             }
         }
+        if (P.tma_c && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // slabs stay live until read
     }
     if (CS > 1)
         cluster_sync_all();  // no peer may still multicast into / arrive on this CTA
     else
         __syncthreads();
-    if (warp == 2) {
+    if (warp == kWarpAlloc) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
     }
@@ -643,13 +685,37 @@ static bool make_map(CUtensorMap* map, const void* base, long long inner, long l
     return r == CUDA_SUCCESS;
 }
 
+static bool make_map_sw(CUtensorMap* map, const void* base, long long inner, long long outer, long long ld, int b1,
+                        long long s1, int b2, long long s2, int box_inner, int box_outer, CUtensorMapSwizzle sw) {
+    EncodeFn fn = encode_fn();
+    if (!fn) return false;
+    const long long plane = ld * outer;
+    if (b1 <= 1 || s1 == 0) s1 = plane;
+    if (b2 <= 1 || s2 == 0) s2 = s1 * (b1 > 0 ? b1 : 1);
+    cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)(b1 > 0 ? b1 : 1), (cuuint64_t)(b2 > 0 ? b2 : 1)};
+    cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(s1 * 2), (cuuint64_t)(s2 * 2)};
+    cuuint32_t box[4] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+           CUDA_SUCCESS;
+}
+
+static bool no_tma_store() {
+    static const bool v = [] {
+        const char* e = std::getenv("AH_GEMM_TMA_STORE");
+        return e && std::string(e) == "0";
+    }();
+    return v;
+}
+
 template <int BN, int STAGES>
 static size_t smem_bytes() {
-    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem;
+    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem + 1024 + kEpiWarps * 2 * 2048;
 }
 
 template <int BN, int STAGES, int CS>
-static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const Params& P, int grid,
+static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const Params& P, int grid,
                               cudaStream_t stream) {
     const size_t sm = smem_bytes<BN, STAGES>();
     static bool configured = false;
@@ -659,7 +725,7 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const 
         configured = true;
     }
     if (CS == 1) {
-        gemm_kernel<BN, STAGES, CS><<<grid, kThreads, sm, stream>>>(a, b, P);
+        gemm_kernel<BN, STAGES, CS><<<grid, kThreads, sm, stream>>>(a, b, c, P);
         return launched(1);
     }
     cudaLaunchConfig_t cfg{};
@@ -674,7 +740,7 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES, CS>, a, b, P);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES, CS>, a, b, c, P);
     launched(1);
     return e != cudaSuccess ? e : cudaGetLastError();
 }
@@ -788,6 +854,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         P.vec16_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
                       g.aux_s2 % 8 == 0;
         P.staged = 0;
+        static const bool no_store = [] {
+            const char* e = std::getenv("AH_GEMM_DEBUG_NO_STORE");
+            return e && std::string(e) == "1";
+        }();
+        P.dbg_no_store = no_store;
         P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
         P.vec16_res = (reinterpret_cast<uintptr_t>(g.residual) % 16 == 0) && g.ld_res % 8 == 0 && g.res_s1 % 8 == 0 &&
                       g.res_s2 % 8 == 0;
@@ -810,6 +881,14 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
                           ? make_map(&mb, g.B, g.N, g.K, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, 64)
                           : make_map(&mb, g.B, g.K, g.N, g.ldb, P.batch1, g.b_s1, P.batch2, g.b_s2, 64, BN / CS);
     if (!ok_a || !ok_b) return cudaErrorInvalidValue;
+    // bf16 C through TMA bulk stores (16-byte aligned base and strides; OOB rows/cols clipped)
+    CUtensorMap mc;
+    std::memset(&mc, 0, sizeof(mc));
+    P.tma_c = 0;
+    if (!g.c_f32 && (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % 8 == 0 && (P.batch1 == 1 || g.c_s1 % 8 == 0) &&
+        (P.batch2 == 1 || g.c_s2 % 8 == 0) && !P.dbg_no_store && !no_tma_store())
+        P.tma_c = make_map_sw(&mc, g.C, g.N, g.M, g.ldc, P.batch1, g.c_s1, P.batch2, g.c_s2, 32, 32,
+                              CU_TENSOR_MAP_SWIZZLE_64B) ? 1 : 0;
     const int max_clusters = kNumSMs / CS;
     int grid = (P.num_tiles < max_clusters ? P.num_tiles : max_clusters) * CS;
     if (max_ctas > 0 && grid > max_ctas) grid = (max_ctas / CS) * CS;
@@ -826,11 +905,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     }
     cudaError_t e;
     if (BN == 256)
-        e = CS == 2 ? launch_cfg<256, 4, 2>(ma, mb, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, P, grid, stream);
+        e = CS == 2 ? launch_cfg<256, 4, 2>(ma, mb, mc, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, mc, P, grid, stream);
     else if (BN == 128)
-        e = launch_cfg<128, 6, 1>(ma, mb, P, grid, stream);
+        e = launch_cfg<128, 6, 1>(ma, mb, mc, P, grid, stream);
     else
-        e = launch_cfg<64, 8, 1>(ma, mb, P, grid, stream);
+        e = launch_cfg<64, 8, 1>(ma, mb, mc, P, grid, stream);
     if (timed) {
         cudaEventRecord(tb, stream);
         std::lock_guard<std::mutex> lk(timing().mu);
