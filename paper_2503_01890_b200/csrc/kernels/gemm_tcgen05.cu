@@ -73,6 +73,10 @@ struct Params {
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
     int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE=1: skip the epilogue (profiling only)
     int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
+    int sk;                   // stream-K work split (CS == 1, non-causal)
+    float* sk_ws;             // [grid][BM][BN] fp32 prefix partials
+    unsigned* sk_flags;       // [grid] release flags (== sk_epoch when the partial is ready)
+    unsigned sk_epoch;
 };
 
 // ---------------------------------------------------------------------------------------
@@ -177,6 +181,7 @@ __device__ __forceinline__ float gelu_tanh(float x) {
 struct Tile {
     int z1, z2, tm, tn, kb0, kb1;
     bool skip;
+    int role;  // 0: whole tile, 1: stream-K prefix (partial -> workspace), 2: stream-K suffix (adds it)
 };
 
 __device__ __forceinline__ Tile decode_at(const Params& P, int z, int tm, int tn, int BN) {
@@ -213,6 +218,46 @@ __device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int cran
     const int rem = ct - z * per_z;
     const int g = rem / P.tiles_n;
     return decode_at(P, z, g * CS + crank, rem - g * P.tiles_n, BN);
+}
+
+// ---- work assignment -------------------------------------------------------------------
+// Data-parallel: cluster tiles strided over the grid (L2-friendly: concurrently running CTAs
+// share A panels). Tail split (P.sk, CS == 1): the W full waves stay data-parallel and each of
+// the remaining `tail` tiles (2 * tail <= grid) is split in two K halves on CTAs 2u (prefix,
+// processed FIRST, partial -> workspace slot + release flag) and 2u + 1 (suffix, processed
+// LAST, adds the partial before its epilogue), so the last wave costs half a tile instead of
+// a whole one (512 tiles on 148 SMs: 3.5 instead of 4 tile times).
+template <int CS>
+__device__ __forceinline__ int num_segments(const Params& P) {
+    const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    if (!P.sk) return cid < P.num_tiles ? (P.num_tiles - 1 - cid) / ncl + 1 : 0;
+    const int G = gridDim.x, waves = P.num_tiles / G, tail = P.num_tiles - waves * G;
+    return waves + ((int)blockIdx.x < 2 * tail ? 1 : 0);
+}
+
+template <int CS>
+__device__ __forceinline__ Tile segment(const Params& P, int i, int BN, int crank) {
+    if (!P.sk) {
+        Tile T = decode<CS>(P, blockIdx.x / CS + i * (gridDim.x / CS), BN, crank);
+        T.role = 0;
+        return T;
+    }
+    const int G = gridDim.x, c = blockIdx.x, waves = P.num_tiles / G, tail = P.num_tiles - waves * G;
+    const bool unit = c < 2 * tail;
+    const bool prefix = unit && (c & 1) == 0;
+    int t, k0 = 0, k1 = P.k_blocks, role = 0;
+    if (prefix && i == 0) {
+        t = waves * G + c / 2, k1 = P.k_blocks / 2, role = 1;
+    } else if (unit && !prefix && i == waves) {
+        t = waves * G + c / 2, k0 = P.k_blocks / 2, role = 2;
+    } else {
+        t = c + (i - (prefix ? 1 : 0)) * G;
+    }
+    Tile T = decode<1>(P, t, BN, 0);
+    T.kb0 = k0;
+    T.kb1 = k1;
+    T.role = role;
+    return T;
 }
 
 __device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
@@ -294,8 +339,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             // ===== TMA producer =====
             int stage = 0;
             uint32_t phase = 0;
-            for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
-                const Tile T = decode<CS>(P, ct, BN, crank);
+            const int nseg = num_segments<CS>(P);
+            for (int si = 0; si < nseg; ++si) {
+                const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -354,8 +400,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
-                const Tile T = decode<CS>(P, ct, BN, crank);
+            const int nseg = num_segments<CS>(P);
+            for (int si = 0; si < nseg; ++si) {
+                const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
                 mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
                 tc_fence_after();
@@ -403,11 +450,22 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         int epi_chunk = 0;  // TMA-store slabs used by this warp (double-buffered)
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int ct = blockIdx.x / CS; ct < P.num_tiles; ct += gridDim.x / CS) {
-            const Tile T = decode<CS>(P, ct, BN, crank);
+        const int nseg = num_segments<CS>(P);
+        for (int si = 0; si < nseg; ++si) {
+            const Tile T = segment<CS>(P, si, BN, crank);
             if (T.skip) continue;
             mbar_wait(smem_u32(&tfull[acc]), acc_phase);
             tc_fence_after();
+            if (T.role == 2) {  // stream-K suffix: wait for the previous CTA's partial of this tile
+                if (warp == 0 && lane == 0) {
+                    unsigned f = 0;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + blockIdx.x - 1) : "memory");
+                        if (f != P.sk_epoch) __nanosleep(64);
+                    } while (f != P.sk_epoch);
+                }
+                asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+            }
             const int m_base = T.tm * BM + q * 32;
             const long long zc = (long long)T.z1 * P.c_s1 + (long long)T.z2 * P.c_s2;
             const long long zr = (long long)T.z1 * P.res_s1 + (long long)T.z2 * P.res_s2;
@@ -419,6 +477,23 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 tmem_ld32(tmem_base + (uint32_t(q * 32) << 16) + acc * BN + c * 32, v);
                 const int n0 = T.tn * BN + c * 32;
                 if (rows <= 0 || n0 >= P.N) continue;  // warp-uniform
+                if (T.role != 0) {  // stream-K: raw fp32 accumulator row chunk <-> workspace slot
+                    const unsigned slot_cta = T.role == 1 ? blockIdx.x : blockIdx.x - 1;
+                    float4* s4 = reinterpret_cast<float4*>(P.sk_ws + ((size_t)slot_cta * BM + q * 32 + lane) * BN + c * 32);
+                    if (T.role == 1) {
+#pragma unroll
+                        for (int w = 0; w < 8; ++w) s4[w] = make_float4(v[4 * w], v[4 * w + 1], v[4 * w + 2], v[4 * w + 3]);
+                        continue;
+                    }
+#pragma unroll
+                    for (int w = 0; w < 8; ++w) {
+                        const float4 x = s4[w];
+                        v[4 * w] += x.x;
+                        v[4 * w + 1] += x.y;
+                        v[4 * w + 2] += x.z;
+                        v[4 * w + 3] += x.w;
+                    }
+                }
                 if (P.dbg_no_store) continue;  // diagnostics: main loop only
                 if (!P.staged) {  // bf16 output: each thread owns its row's 32 columns
                     const int m = m_base + lane;
@@ -630,6 +705,13 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (T.role == 1) {  // publish the prefix partial for the next CTA
+                asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
+                if (warp == 0 && lane == 0) {
+                    __threadfence();
+                    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(P.sk_flags + blockIdx.x), "r"(P.sk_epoch) : "memory");
+                }
+            }
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -871,7 +953,37 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         const char* e = std::getenv("AH_GEMM_CLUSTER");
         return e && std::string(e) == "1";
     }();
-    const int CS = (!no_cluster && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
+    // Stream-K when the data-parallel tile count fills the last wave poorly (e.g. 512 tiles on
+    // 148 SMs -> 86 % of 4 waves): every CTA then gets the same number of k-block iterations.
+    static const bool no_sk = [] {
+        const char* e = std::getenv("AH_GEMM_STREAMK");
+        return e && std::string(e) == "0";
+    }();
+    {
+        const int waves = (P.num_tiles + kNumSMs - 1) / kNumSMs;
+        const double eff = (double)P.num_tiles / ((double)waves * kNumSMs);
+        const int tail = P.num_tiles - (P.num_tiles / kNumSMs) * kNumSMs;
+        P.sk = (!no_sk && g.causal == kCausalNone && P.num_tiles >= kNumSMs && eff < 0.9 && BN == 256 && tail > 0 &&
+                2 * tail <= kNumSMs && P.k_blocks >= 64) ? 1 : 0;  // measured: +4% at K=8192, -2% at K=2048
+    }
+    if (P.sk) {
+        static std::mutex mu;
+        static float* ws = nullptr;
+        static unsigned* flags = nullptr;
+        static unsigned epoch = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!ws) {
+            if (cudaMalloc(&ws, (size_t)kNumSMs * BM * 256 * 4) != cudaSuccess ||
+                cudaMalloc(&flags, kNumSMs * sizeof(unsigned)) != cudaSuccess ||
+                cudaMemset(flags, 0, kNumSMs * sizeof(unsigned)) != cudaSuccess)
+                return cudaErrorMemoryAllocation;
+        }
+        P.sk_ws = ws;
+        P.sk_flags = flags;
+        P.sk_epoch = ++epoch;
+        if (P.sk_epoch == 0) P.sk_epoch = ++epoch;  // flags start at 0
+    }
+    const int CS = (!no_cluster && !P.sk && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
     if (CS > 1) P.num_tiles = ((P.tiles_m + CS - 1) / CS) * P.tiles_n * P.batch1 * P.batch2;
     CUtensorMap ma, mb;
     const bool ok_a = g.a_mn_major
@@ -890,7 +1002,7 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         P.tma_c = make_map_sw(&mc, g.C, g.N, g.M, g.ldc, P.batch1, g.c_s1, P.batch2, g.c_s2, 32, 32,
                               CU_TENSOR_MAP_SWIZZLE_64B) ? 1 : 0;
     const int max_clusters = kNumSMs / CS;
-    int grid = (P.num_tiles < max_clusters ? P.num_tiles : max_clusters) * CS;
+    int grid = P.sk ? kNumSMs : (P.num_tiles < max_clusters ? P.num_tiles : max_clusters) * CS;
     if (max_ctas > 0 && grid > max_ctas) grid = (max_ctas / CS) * CS;
     cudaEvent_t ta = nullptr, tb = nullptr;
     bool timed = false;

@@ -148,3 +148,19 @@ def test_gemm_gelu_bwd_epilogue(cuda_device, native):
     g = A.float() @ B.float().T
     y.backward(g)
     assert rel_err(out, x.grad) < 1e-2
+
+
+@pytest.mark.parametrize("M,N,K,a_mn,b_mn", [(8192, 2048, 4096, 0, 0), (2048, 8192, 4096, 1, 1), (4096, 2560, 4160, 0, 1)])
+def test_gemm_stream_k_shapes(cuda_device, native, M, N, K, a_mn, b_mn):
+    """Tile counts that fill the last wave poorly take the tail split (K halves handed
+    between CTAs through a workspace); results must match the reference incl. epilogues."""
+    from paper_2503_01890_b200.gemm import gemm
+    A, B, a_arg, b_arg = operands(M, N, K, a_mn, b_mn, seed=M + N)
+    bias = torch.randn(N, device="cuda").bfloat16()
+    res = torch.randn(M, N, device="cuda").bfloat16()
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    for _ in range(2):  # second launch reuses the workspace / flags with a new epoch
+        gemm(a_arg, b_arg, C, a_mn=bool(a_mn), b_mn=bool(b_mn), bias=bias, residual=res)
+    torch.cuda.synchronize()
+    ref = A.float() @ B.float().T + bias.float() + res.float()
+    assert rel_err(C, ref) < 1e-2
