@@ -26,6 +26,15 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return f32_to_bf16_bits(lo) | (f32_to_bf16_bits(hi) << 16);
 }
 
+// Hardware round-to-nearest-even pack (one cvt per pair). Same bits as pack_bf16x2 for every
+// non-NaN input; NaNs come out canonical. For kernel epilogues whose outputs are not part of a
+// bit-exact CPU contract (GEMM / attention activations).
+__device__ __forceinline__ uint32_t pack_bf16x2_rn(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
 // Streaming 128-bit accesses: read-once data bypasses L1 allocation.
 __device__ __forceinline__ uint4 ld_stream_u4(const void* p) {
     uint4 r;

@@ -71,8 +71,9 @@ struct Params {
     int vec16_c, vec16_aux;  // 16-byte rows (direct path)
     int staged;              // smem-transposed epilogue (fp32 outputs)
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
-    int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE=1: skip the epilogue (profiling only)
+    int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE (profiling only): 1 no epilogue, 2 no C store, 3 packs only
     int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
+    int fast;                 // tma_c, alpha 1, beta 0, N % BN == 0, 16-byte operand rows: lean epilogue
     int sk;                   // stream-K work split (CS == 1, non-causal)
     float* sk_ws;             // [grid][BM][BN] fp32 prefix partials
     unsigned* sk_flags;       // [grid] release flags (== sk_epoch when the partial is ready)
@@ -260,34 +261,60 @@ __device__ __forceinline__ Tile segment(const Params& P, int i, int BN, int cran
     return T;
 }
 
-__device__ __forceinline__ void tma_load_4d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                               int c2, int c3, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask)
-        : "memory");
-}
-__device__ __forceinline__ void tc_commit_mc(uint32_t bar, uint16_t mask) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-                 "h"(mask)
-                 : "memory");
-}
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
     return r;
 }
+// ---- CTA pair (cta_group::2): one M=256 MMA over the two CTAs' smem, issued by rank 0 ----
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+// TMA into this CTA's smem, completing bytes on the (possibly peer) barrier `bar` (cluster address)
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                 int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+// arrive on the barrier at the same smem offset in both CTAs of the pair
+__device__ __forceinline__ void tc_commit_pair(uint32_t bar) {
+    asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+                 "h"((uint16_t)3)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_bar) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_bar) : "memory");
+}
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// CS == 2: CTA pair. Each CTA stages its own 128 A rows and half (BN/2 rows) of the B tile;
+// rank 0 issues tcgen05.mma.cta_group::2 with M = 256, which reads both CTAs' smem and writes
+// each CTA's 128 accumulator rows into its own TMEM. Rank 0's full barrier collects both CTAs'
+// TMA bytes; its commits arrive on both CTAs' empty / tmem-full barriers (multicast); both
+// CTAs' epilogues release the accumulator on rank 0's tmem-empty barrier. Per SM, the MMA
+// reads 32 KB of smem per k-block instead of 48 KB.
 template <int BN, int STAGES, int CS>
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
             const __grid_constant__ CUtensorMap tmC, const Params P) {
+    static_assert(CS == 1 || (CS == 2 && BN == 256), "CTA pair: BN = 256");
+    constexpr bool kPair = CS == 2;
     constexpr uint32_t A_BYTES = BM * BK * 2;
-    constexpr uint32_t B_BYTES = BN * BK * 2;
+    constexpr uint32_t B_BYTES = (BN / CS) * BK * 2;  // this CTA's part of the B tile
     constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
@@ -312,19 +339,25 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(smem_u32(&full[s]), 1);
-            mbar_init(smem_u32(&empty[s]), CS);  // one MMA commit per cluster CTA
+            mbar_init(smem_u32(&empty[s]), 1);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(smem_u32(&tfull[a]), 1);
-            mbar_init(smem_u32(&tempty[a]), kEpiWarps);
+            mbar_init(smem_u32(&tempty[a]), kEpiWarps * CS);  // pair: both CTAs' epilogues (rank 0's)
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     if (warp == kWarpAlloc) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(2 * BN));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        if (kPair) {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                         "r"(2 * BN));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                         "r"(2 * BN));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
     }
     tc_fence_before();
     if (CS > 1)
@@ -345,11 +378,35 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 if (T.skip) continue;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
                     mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-                    const uint32_t fb = smem_u32(&full[stage]);
-                    mbar_expect_tx(fb, STAGE_BYTES);
                     const uint32_t a_dst = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_dst = smem_u32(sB + stage * B_BYTES);
                     const int k0 = kb * BK;
+                    if (kPair) {  // both CTAs' bytes complete on rank 0's full barrier
+                        const uint32_t fb = mapa_rank(smem_u32(&full[stage]), 0);
+                        if (crank == 0) mbar_expect_tx(smem_u32(&full[stage]), 2 * STAGE_BYTES);
+                        if (!P.a_mn) {
+                            tma_load_4d_pair(a_dst, &tmA, fb, k0, T.tm * BM, T.z1, T.z2);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < BM / 64; ++j)
+                                tma_load_4d_pair(a_dst + j * (64 * BK * 2), &tmA, fb, T.tm * BM + j * 64, k0, T.z1, T.z2);
+                        }
+                        if (!P.b_mn) {
+                            tma_load_4d_pair(b_dst, &tmB, fb, k0, T.tn * BN + crank * (BN / 2), T.z1, T.z2);
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < BN / 128; ++jj)
+                                tma_load_4d_pair(b_dst + jj * (64 * BK * 2), &tmB, fb, T.tn * BN + crank * (BN / 2) + jj * 64,
+                                                 k0, T.z1, T.z2);
+                        }
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                        continue;
+                    }
+                    const uint32_t fb = smem_u32(&full[stage]);
+                    mbar_expect_tx(fb, STAGE_BYTES);
                     if (!P.a_mn) {
                         tma_load_4d(a_dst, &tmA, fb, k0, T.tm * BM, T.z1, T.z2);
                     } else {
@@ -357,27 +414,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int j = 0; j < BM / 64; ++j)
                             tma_load_4d(a_dst + j * (64 * BK * 2), &tmA, fb, T.tm * BM + j * 64, k0, T.z1, T.z2);
                     }
-                    if (CS == 1) {
-                        if (!P.b_mn) {
-                            tma_load_4d(b_dst, &tmB, fb, k0, T.tn * BN, T.z1, T.z2);
-                        } else {
+                    if (!P.b_mn) {
+                        tma_load_4d(b_dst, &tmB, fb, k0, T.tn * BN, T.z1, T.z2);
+                    } else {
 #pragma unroll
-                            for (int j = 0; j < BN / 64; ++j)
-                                tma_load_4d(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2);
-                        }
-                    } else {  // this rank's 1/CS of the shared B tile, multicast to the cluster
-                        constexpr uint16_t mask = (1u << CS) - 1;
-                        if (!P.b_mn) {
-                            tma_load_4d_mc(b_dst + crank * (BN / CS) * 128, &tmB, fb, k0, T.tn * BN + crank * (BN / CS),
-                                           T.z1, T.z2, mask);
-                        } else {
-#pragma unroll
-                            for (int jj = 0; jj < BN / 64 / CS; ++jj) {
-                                const int j = crank * (BN / 64 / CS) + jj;
-                                tma_load_4d_mc(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2,
-                                               mask);
-                            }
-                        }
+                        for (int j = 0; j < BN / 64; ++j)
+                            tma_load_4d(b_dst + j * (64 * BK * 2), &tmB, fb, T.tn * BN + j * 64, k0, T.z1, T.z2);
                     }
                     if (++stage == STAGES) {
                         stage = 0;
@@ -387,10 +429,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
         }
     } else if (warp == kWarpMMA) {
-        if (lane == 0) {
-            // ===== MMA issuer =====
+        if (lane == 0 && crank == 0) {
+            // ===== MMA issuer (pair: rank 0 only) =====
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(P.a_mn) << 15) |
-                                   (uint32_t(P.b_mn) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+                                   (uint32_t(P.b_mn) << 16) | (uint32_t(BN >> 3) << 17) | (uint32_t((BM * CS) >> 4) << 24);
             // K-major: rows of 128 B, 8-row atoms 1024 B apart; K step of 16 = +32 B.
             // MN-major: 64-element (128 B) chunks BK rows deep (LBO = 64*BK*2 B apart), 8-row
             // K groups 1024 B apart; K step of 16 = +2048 B.
@@ -416,18 +458,24 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int k = 0; k < BK / 16; ++k) {
                         const uint64_t ad = smem_desc(a_addr + k * a_kstep, a_lbo, a_sbo);
                         const uint64_t bd = smem_desc(b_addr + k * b_kstep, b_lbo, b_sbo);
-                        tc_mma(d_tmem, ad, bd, idesc, (kb > T.kb0 || k > 0) ? 1u : 0u);
+                        if (kPair)
+                            tc_mma_pair(d_tmem, ad, bd, idesc, (kb > T.kb0 || k > 0) ? 1u : 0u);
+                        else
+                            tc_mma(d_tmem, ad, bd, idesc, (kb > T.kb0 || k > 0) ? 1u : 0u);
                     }
-                    if (CS == 1)
+                    if (kPair)
+                        tc_commit_pair(smem_u32(&empty[stage]));
+                    else
                         tc_commit(smem_u32(&empty[stage]));
-                    else  // the stage holds peers' B slices: free it in every cluster CTA
-                        tc_commit_mc(smem_u32(&empty[stage]), (uint16_t)((1u << CS) - 1));
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                tc_commit(smem_u32(&tfull[acc]));
+                if (kPair)
+                    tc_commit_pair(smem_u32(&tfull[acc]));
+                else
+                    tc_commit(smem_u32(&tfull[acc]));
                 if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
@@ -494,7 +542,72 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         v[4 * w + 3] += x.w;
                     }
                 }
-                if (P.dbg_no_store) continue;  // diagnostics: main loop only
+                if (P.dbg_no_store == 1) continue;  // diagnostics: main loop only
+                if (P.fast && rows == 32) {
+                    // Lean path for whole 32 x 32 chunks: vector operand loads, hardware bf16
+                    // packs, one TMA store. (Its instruction count paces the MMAs: every issue
+                    // slot spent here is shared with the single-thread MMA issuer.)
+                    const int m = m_base + lane;
+                    if (P.epi & kEpiBias) {
+                        const uint4* b4 = reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(P.bias) + n0);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) add8(v, 8 * w, b4[w]);
+                    }
+                    if (P.epi & (kEpiAux | kEpiGeluBwd)) {
+                        uint4* a4 = reinterpret_cast<uint4*>(P.aux + za + (long long)m * P.ld_aux + n0);
+                        if (P.epi & kEpiGeluBwd) {
+#pragma unroll
+                            for (int w = 0; w < 4; ++w) {
+                                const uint4 q4 = a4[w];
+                                const uint32_t u[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                                for (int e = 0; e < 8; ++e)
+                                    v[8 * w + e] *= gelu_grad(__uint_as_float((e & 1) ? (u[e >> 1] & 0xffff0000u) : (u[e >> 1] << 16)));
+                            }
+                        } else {
+#pragma unroll
+                            for (int w = 0; w < 4; ++w)
+                                a4[w] = make_uint4(pack_bf16x2_rn(v[8 * w], v[8 * w + 1]), pack_bf16x2_rn(v[8 * w + 2], v[8 * w + 3]),
+                                                   pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
+                        }
+                    }
+                    if ((P.epi & kEpiGelu) && !(P.epi & kEpiGeluBwd)) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+                    }
+                    if (P.epi & kEpiResidual) {
+                        const uint4* r4 = reinterpret_cast<const uint4*>(P.res + zr + (long long)m * P.ld_res + n0);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w) add8(v, 8 * w, r4[w]);
+                    }
+                    uint8_t* slab = cstage + (warp * 2 + (epi_chunk & 1)) * 2048;
+                    if (P.dbg_no_store == 3) {  // diagnostics: packs only
+                        uint32_t x = 0;
+#pragma unroll
+                        for (int w = 0; w < 16; ++w) x ^= pack_bf16x2_rn(v[2 * w], v[2 * w + 1]);
+                        if (x == 0x12345678u) *reinterpret_cast<uint32_t*>(slab) = x;
+                        continue;
+                    }
+                    if (epi_chunk >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    __syncwarp();
+#pragma unroll
+                    for (int w = 0; w < 4; ++w)
+                        *reinterpret_cast<uint4*>(slab + lane * 64 + ((w ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(pack_bf16x2_rn(v[8 * w], v[8 * w + 1]), pack_bf16x2_rn(v[8 * w + 2], v[8 * w + 3]),
+                                       pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0 && P.dbg_no_store != 2) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tmC)),
+                            "r"(smem_u32(slab)), "r"(n0), "r"(m_base), "r"(T.z1), "r"(T.z2)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++epi_chunk;
+                    continue;
+                }
                 if (!P.staged) {  // bf16 output: each thread owns its row's 32 columns
                     const int m = m_base + lane;
                     const bool row_live = m < P.M;
@@ -505,8 +618,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] = 0.f;
                 } else {
+                if (P.alpha != 1.f) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] *= P.alpha;
+                    for (int j = 0; j < 32; ++j) v[j] *= P.alpha;
+                }
                 if (P.beta != 0.f) {
                     if (P.c_f32) {
                         const float* cp = static_cast<const float*>(P.C) + c_off + n0;
@@ -559,8 +674,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         uint4* a4 = reinterpret_cast<uint4*>(ap);
 #pragma unroll
                         for (int w = 0; w < 4; ++w)
-                            a4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
-                                               pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                            a4[w] = make_uint4(pack_bf16x2_rn(v[8 * w], v[8 * w + 1]), pack_bf16x2_rn(v[8 * w + 2], v[8 * w + 3]),
+                                               pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
                     } else {
                         #pragma unroll
                         for (int j = 0; j < 32; ++j) if (n0 + j < P.N) ap[j] = (uint16_t)f32_to_bf16_bits(v[j]);
@@ -591,8 +706,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int w = 0; w < 4; ++w) {
                         const int chunk = w ^ ((lane >> 1) & 3);
                         *reinterpret_cast<uint4*>(slab + lane * 64 + chunk * 16) =
-                            make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
-                                       pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                            make_uint4(pack_bf16x2_rn(v[8 * w], v[8 * w + 1]), pack_bf16x2_rn(v[8 * w + 2], v[8 * w + 3]),
+                                       pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
                     }
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
@@ -623,8 +738,8 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         uint4* c4 = reinterpret_cast<uint4*>(cp);
 #pragma unroll
                         for (int w = 0; w < 4; ++w)
-                            c4[w] = make_uint4(pack_bf16x2(v[8 * w], v[8 * w + 1]), pack_bf16x2(v[8 * w + 2], v[8 * w + 3]),
-                                               pack_bf16x2(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2(v[8 * w + 6], v[8 * w + 7]));
+                            c4[w] = make_uint4(pack_bf16x2_rn(v[8 * w], v[8 * w + 1]), pack_bf16x2_rn(v[8 * w + 2], v[8 * w + 3]),
+                                               pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
                     } else {
                         #pragma unroll
                         for (int j = 0; j < 32; ++j) if (n0 + j < P.N) cp[j] = (uint16_t)f32_to_bf16_bits(v[j]);
@@ -671,7 +786,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             for (int k = 0; k < 4; ++k)
                                 if (k < ncols) x[k] *= gelu_grad(bf16_bits_to_f32(ap[k]));
                         } else if (vec && P.vec_aux) {
-                            *reinterpret_cast<uint2*>(ap) = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
+                            *reinterpret_cast<uint2*>(ap) = make_uint2(pack_bf16x2_rn(x[0], x[1]), pack_bf16x2_rn(x[2], x[3]));
                         } else {
                             for (int k = 0; k < ncols; ++k) ap[k] = (uint16_t)f32_to_bf16_bits(x[k]);
                         }
@@ -695,7 +810,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     } else {
                         uint16_t* cp = static_cast<uint16_t*>(P.C) + ci;
                         if (vec)
-                            *reinterpret_cast<uint2*>(cp) = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
+                            *reinterpret_cast<uint2*>(cp) = make_uint2(pack_bf16x2_rn(x[0], x[1]), pack_bf16x2_rn(x[2], x[3]));
                         else
                             for (int k = 0; k < ncols; ++k) cp[k] = (uint16_t)f32_to_bf16_bits(x[k]);
                     }
@@ -704,7 +819,12 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+            if (lane == 0) {
+                if (kPair)
+                    mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[acc]), 0));
+                else
+                    mbar_arrive(smem_u32(&tempty[acc]));
+            }
             if (T.role == 1) {  // publish the prefix partial for the next CTA
                 asm volatile("bar.sync 1, %0;" ::"r"(kEpiWarps * 32) : "memory");
                 if (warp == 0 && lane == 0) {
@@ -725,7 +845,10 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         __syncthreads();
     if (warp == kWarpAlloc) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+        if (kPair)
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
+        else
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(2 * BN));
     }
 }
 
@@ -791,15 +914,15 @@ static bool no_tma_store() {
     return v;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CS>
 static size_t smem_bytes() {
-    return 1024 + STAGES * (size_t)(BM * BK * 2 + BN * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem + 1024 + kEpiWarps * 2 * 2048;
+    return 1024 + STAGES * (size_t)(BM * BK * 2 + (BN / CS) * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem + 1024 + kEpiWarps * 2 * 2048;
 }
 
 template <int BN, int STAGES, int CS>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c, const Params& P, int grid,
                               cudaStream_t stream) {
-    const size_t sm = smem_bytes<BN, STAGES>();
+    const size_t sm = smem_bytes<BN, STAGES, CS>();
     static bool configured = false;
     if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(gemm_kernel<BN, STAGES, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -936,9 +1059,9 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         P.vec16_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
                       g.aux_s2 % 8 == 0;
         P.staged = 0;
-        static const bool no_store = [] {
+        static const int no_store = [] {  // 1: no epilogue, 2: no TMA store, 3: packs only
             const char* e = std::getenv("AH_GEMM_DEBUG_NO_STORE");
-            return e && std::string(e) == "1";
+            return e ? std::atoi(e) : 0;
         }();
         P.dbg_no_store = no_store;
         P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
@@ -946,9 +1069,9 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
                       g.res_s2 % 8 == 0;
     }
 
-    // Clusters of 2 CTAs share (multicast) the B tile of two adjacent M tiles: every SM then
-    // pulls 16 KB instead of 32 KB of B per stage from L2 (the linear-layer GEMMs are L2-bound
-    // at one CTA per tile). Causal tiles have per-tile K ranges, so they stay unclustered.
+    // CTA pairs (cta_group::2, M = 256 over two adjacent M tiles sharing the B tile): each SM
+    // stages and the MMA reads half of B, so smem traffic per k-block drops from 48 to 32 KB
+    // and L2 -> SM traffic for B halves. Causal tiles have per-tile K ranges: unpaired.
     static const bool no_cluster = [] {
         const char* e = std::getenv("AH_GEMM_CLUSTER");
         return e && std::string(e) == "1";
@@ -998,9 +1121,12 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     std::memset(&mc, 0, sizeof(mc));
     P.tma_c = 0;
     if (!g.c_f32 && (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % 8 == 0 && (P.batch1 == 1 || g.c_s1 % 8 == 0) &&
-        (P.batch2 == 1 || g.c_s2 % 8 == 0) && !P.dbg_no_store && !no_tma_store())
+        (P.batch2 == 1 || g.c_s2 % 8 == 0) && P.dbg_no_store != 1 && !no_tma_store())
         P.tma_c = make_map_sw(&mc, g.C, g.N, g.M, g.ldc, P.batch1, g.c_s1, P.batch2, g.c_s2, 32, 32,
                               CU_TENSOR_MAP_SWIZZLE_64B) ? 1 : 0;
+    P.fast = P.tma_c && g.alpha == 1.f && g.beta == 0.f && P.N % BN == 0 &&
+             (!(g.epilogue & kEpiBias) || P.vec_bias) && (!(g.epilogue & kEpiResidual) || P.vec16_res) &&
+             (!(g.epilogue & (kEpiAux | kEpiGeluBwd)) || P.vec16_aux);
     const int max_clusters = kNumSMs / CS;
     int grid = P.sk ? kNumSMs : (P.num_tiles < max_clusters ? P.num_tiles : max_clusters) * CS;
     if (max_ctas > 0 && grid > max_ctas) grid = (max_ctas / CS) * CS;
@@ -1017,7 +1143,7 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     }
     cudaError_t e;
     if (BN == 256)
-        e = CS == 2 ? launch_cfg<256, 4, 2>(ma, mb, mc, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, mc, P, grid, stream);
+        e = CS == 2 ? launch_cfg<256, 6, 2>(ma, mb, mc, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, mc, P, grid, stream);
     else if (BN == 128)
         e = launch_cfg<128, 6, 1>(ma, mb, mc, P, grid, stream);
     else
