@@ -277,6 +277,91 @@ __global__ void ce_kernel(uint16_t* logits, const int* __restrict__ tgt, float* 
     }
 }
 
+// Register-resident variant: the row (ld <= kCeThreads * 8 * kCeVec bf16) is read once with
+// 16-byte loads into registers, each thread reduces its own (max, sum) pair, one block combine,
+// and dlogits are written from the registers: 2 B read + 2 B written per logit (the three-pass
+// kernel above re-reads the row three times with 2-byte loads).
+constexpr int kCeThreads = 512, kCeVec = 13;
+__device__ __forceinline__ uint32_t bf16x2_max(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("max.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
+}
+__global__ void __launch_bounds__(kCeThreads, 1)
+ce_reg_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__ loss, int V, int ld, float dscale) {
+    __shared__ float red_m[32], red_s[32];
+    constexpr uint32_t kNegInf2 = 0xff80ff80u;  // two bf16 -inf: padding / out-of-row lanes
+    const int row = blockIdx.x;
+    uint16_t* lr = logits + (size_t)row * ld;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nvec = ld >> 3;
+    const int t = tgt[row];
+    const float tl = bf16_bits_to_f32(lr[t]);  // read before any thread overwrites the row
+    uint4 r[kCeVec];
+#pragma unroll
+    for (int i = 0; i < kCeVec; ++i) {
+        const int idx = threadIdx.x + i * kCeThreads;
+        r[i] = idx < nvec ? ldg16(lr + (size_t)idx * 8) : make_uint4(kNegInf2, kNegInf2, kNegInf2, kNegInf2);
+        if (idx < nvec && idx * 8 + 8 > V) {  // padding columns (>= V) never count
+            uint32_t* u = reinterpret_cast<uint32_t*>(&r[i]);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+                if (idx * 8 + e >= V) u[e >> 1] = (e & 1) ? ((u[e >> 1] & 0xffffu) | 0xff800000u) : ((u[e >> 1] & 0xffff0000u) | 0xff80u);
+        }
+    }
+    uint32_t m2 = kNegInf2;
+#pragma unroll
+    for (int i = 0; i < kCeVec; ++i)
+        m2 = bf16x2_max(bf16x2_max(m2, bf16x2_max(r[i].x, r[i].y)), bf16x2_max(r[i].z, r[i].w));
+    float m = fmaxf(bf16_bits_to_f32(m2 & 0xffffu), bf16_bits_to_f32(m2 >> 16));
+    float sum = 0.f;
+    if (m != -INFINITY) {
+#pragma unroll
+        for (int i = 0; i < kCeVec; ++i) {
+            float f[8];
+            unpack8(r[i], f);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) sum += __expf(f[e] - m);
+        }
+    }
+    // block combine of (m, sum) pairs
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const float mo = __shfl_xor_sync(0xffffffffu, m, o), so = __shfl_xor_sync(0xffffffffu, sum, o);
+        const float mn = fmaxf(m, mo);
+        sum = (m == -INFINITY ? 0.f : sum * __expf(m - mn)) + (mo == -INFINITY ? 0.f : so * __expf(mo - mn));
+        m = mn;
+    }
+    if (lane == 0) {
+        red_m[w] = m;
+        red_s[w] = sum;
+    }
+    __syncthreads();
+    float M = red_m[0];
+    for (int q = 1; q < kCeThreads / 32; ++q) M = fmaxf(M, red_m[q]);
+    float S = 0.f;
+    for (int q = 0; q < kCeThreads / 32; ++q)
+        if (red_m[q] != -INFINITY) S += red_s[q] * __expf(red_m[q] - M);
+    if (threadIdx.x == 0) loss[row] = M + __logf(S) - tl;
+    const float inv = 1.f / S;
+#pragma unroll
+    for (int i = 0; i < kCeVec; ++i) {
+        const int idx = threadIdx.x + i * kCeThreads;
+        if (idx >= nvec) continue;
+        const int c0 = idx * 8;
+        float f[8];
+        unpack8(r[i], f);
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+            const float d0 = (__expf(f[e] - M) * inv - (c0 + e == t ? 1.f : 0.f)) * dscale;
+            const float d1 = (__expf(f[e + 1] - M) * inv - (c0 + e + 1 == t ? 1.f : 0.f)) * dscale;
+            o[e >> 1] = pack_bf16x2(d0, d1);
+        }
+        *reinterpret_cast<uint4*>(lr + (size_t)c0) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 // dwte[v] += sum over positions of v (ascending order) of dx[pos]; one CTA per distinct token.
 __global__ void embed_bwd_tok_kernel(const uint16_t* __restrict__ dx, const int* __restrict__ uniq,
                                      const int* __restrict__ offs, const int* __restrict__ pos, float* dwte, int h) {
@@ -399,7 +484,10 @@ cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre,
 
 cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
                           cudaStream_t st) {
-    ce_kernel<<<T, 512, 0, st>>>(logits, tgt, loss, V, ld, dscale);
+    if (ld % 8 == 0 && ld <= kCeThreads * 8 * kCeVec && reinterpret_cast<uintptr_t>(logits) % 16 == 0)
+        ce_reg_kernel<<<T, kCeThreads, 0, st>>>(logits, tgt, loss, V, ld, dscale);
+    else
+        ce_kernel<<<T, 512, 0, st>>>(logits, tgt, loss, V, ld, dscale);
     return launched(1);
 }
 
