@@ -141,6 +141,17 @@ int ah_gemm_bf16(const ah_gemm_desc* desc, void* stream);
 int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
                      int32_t heads, int32_t head_dim, void* stream);
 
+/* Flash attention forward (the executor's default): qkv [B, s, 3h] bf16 -> O [B, s, h] bf16 and
+ * lse2 [B, heads, s] fp32, the per-row log2-domain log-sum-exp of the scaled scores. */
+int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int32_t batch, int32_t seq_len,
+                           int32_t heads, int32_t head_dim, void* stream);
+
+/* Flash attention backward: from qkv, O, dO [B, s, h] and lse2 -> dqkv [B, s, 3h] bf16 (dQ, dK,
+ * dV of every head; P recomputed). Scratch (B*heads*s*(s*2 + 4) bytes) is stream-allocated. */
+int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2,
+                           uint16_t* dqkv, int32_t batch, int32_t seq_len, int32_t heads, int32_t head_dim,
+                           void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Training executor: one GPT iteration = hetsim::build_iteration_ops(profile, strategy, k)
  * (proj/core/src/simulator.cpp:91-229) executed on B200 in the per-lane order of

@@ -1,6 +1,8 @@
 // extern "C" test / instrumentation entry for the fused attention forward.
 #include "autohete.h"
+#include "../kernels/gemm.h"
 #include "../kernels/gpt_kernels.h"
+#include <cmath>
 #include "capi_util.h"
 
 extern "C" int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
@@ -11,4 +13,46 @@ extern "C" int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, i
     return ah::cuda_status(ah::gpt::attn_fwd(qkv, P, O, batch, seq_len, heads, head_dim,
                                              1.0f / __builtin_sqrtf((float)head_dim), static_cast<cudaStream_t>(stream)),
                            "ah_attention_fwd");
+}
+
+extern "C" int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int32_t batch, int32_t seq_len,
+                                      int32_t heads, int32_t head_dim, void* stream) {
+    if (!qkv || !O || !lse2) return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_fwd: null argument");
+    if (!ah::gpt::flash_supported(head_dim, seq_len))
+        return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_fwd: needs head_dim 128 and seq_len % 128 == 0");
+    return ah::cuda_status(ah::gpt::flash_fwd(qkv, O, lse2, batch, seq_len, heads, head_dim,
+                                              1.0f / std::sqrt((float)head_dim), static_cast<cudaStream_t>(stream)),
+                           "ah_attention_flash_fwd");
+}
+
+extern "C" int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2,
+                                      uint16_t* dqkv, int32_t batch, int32_t seq_len, int32_t heads, int32_t head_dim,
+                                      void* stream) {
+    if (!qkv || !O || !dO || !lse2 || !dqkv) return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: null argument");
+    if (!ah::gpt::flash_supported(head_dim, seq_len))
+        return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: needs head_dim 128 and seq_len % 128 == 0");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const long long s = seq_len, h = (long long)heads * head_dim, rows = (long long)batch * heads * s;
+    const float scale = 1.0f / std::sqrt((float)head_dim);
+    float* D = nullptr;
+    uint16_t* dS = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&D), rows * 4, st);
+    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dS), rows * s * 2, st);
+    if (e == cudaSuccess)
+        e = ah::gpt::flash_bwd(qkv, O, dO, lse2, D, dS, dqkv, batch, seq_len, heads, head_dim, scale, st);
+    if (e == cudaSuccess) {  // dQ = dS K * scale (causal: K range up to the query tile)
+        ah::gemm::GemmArgs g;
+        g.batch1 = heads;
+        g.batch2 = batch;
+        g.M = s; g.N = head_dim; g.K = s;
+        g.A = dS; g.lda = s; g.a_s1 = s * s; g.a_s2 = (long long)heads * s * s;
+        g.B = qkv + h; g.b_mn_major = 1; g.ldb = 3 * h; g.b_s1 = head_dim; g.b_s2 = s * 3 * h;
+        g.C = dqkv; g.ldc = 3 * h; g.c_s1 = head_dim; g.c_s2 = s * 3 * h;
+        g.alpha = scale;
+        g.causal = ah::gemm::kCausalKUptoM;
+        e = ah::gemm::run(g, st);
+    }
+    if (D) cudaFreeAsync(D, st);
+    if (dS) cudaFreeAsync(dS, st);
+    return ah::cuda_status(e, "ah_attention_flash_bwd");
 }

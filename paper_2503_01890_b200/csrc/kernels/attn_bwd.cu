@@ -284,6 +284,11 @@ bool map4(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint
 
 bool attn_bwd_supported(int hd, int s) { return hd == kHD && s % kT == 0; }
 
+cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st) {
+    attn_bwd_dot_kernel<<<(unsigned)(((long long)B * s * nh + 7) / 8), 256, 0, st>>>(dO, O, D, B, s, nh);
+    return launched(1);
+}
+
 cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const uint16_t* P, float* D,
                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st) {
     if (!attn_bwd_supported(hd, s)) return cudaErrorInvalidValue;

@@ -1,0 +1,587 @@
+// Flash-style causal attention on tcgen05 (sm_100a): forward keeps only O and the per-row
+// log-sum-exp; backward recomputes P from Q, K and the log-sum-exp.
+//
+// Forward, one CTA per (128-query tile, head, sequence), heavy (long causal) tiles first:
+//   S_j = Q K_j^T            tcgen05.mma into a double-buffered TMEM score tile
+//   online softmax            8 warps: thread = query row, warp pair (w, w + 4) splits the 128
+//                             keys of a tile; the pair exchanges its tile max through smem
+//   O += P_j V_j              P_j (bf16) staged in smem as the A operand, O accumulated in TMEM
+// Softmax runs in the log2 domain on raw scores, p = 2^(S * scale * log2e - m * scale * log2e),
+// with lazy rescaling: the running max m only moves (and O / l are rescaled in TMEM) when the
+// tile max exceeds it by more than 2^8, so most tiles touch O only through the MMA. Output
+// O / l and lse2 = m * scale * log2e + log2(l) per row (the backward's softmax statistics).
+//
+// Backward, one CTA per (128-key tile, head, sequence), query tiles i >= key tile:
+//   S_i = Q_i K^T, P_i = 2^(S_i * scale * log2e - lse2_i)     (recomputed, never stored)
+//   dP_i = dO_i V^T; dS_i = P_i * (dP_i - D_i)                (D = rowsum(dO * O))
+//   dV += P_i^T dO_i, dK += dS_i^T Q_i                        (TMEM accumulators)
+// dS_i also goes to HBM for the deterministic dQ = dS K GEMM (no cross-CTA atomics).
+// P_i and dS_i share one smem tile (dS overwrites P once the dV MMA has read it).
+//
+// Operand staging: every tile is a K-major SWIZZLE_128B 128 x 128 bf16 box pair (two 64-column
+// atoms); read as the MN-major operand of its transpose it gives P^T, dS^T, V, dO, Q for free.
+// Warp roles (384 threads): 0 TMA producer, 1 MMA issuer (one thread), 2 TMEM allocator,
+// 4-11 softmax / epilogue. Shapes: head_dim = 128, seq_len % 128 == 0.
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "gpt_kernels.h"
+#include "kernels.h"
+#include "tc_ptx.cuh"
+
+namespace ah {
+namespace gpt {
+namespace {
+
+using namespace ah::tc;
+
+constexpr int kHD = 128, kT = 128;
+constexpr uint32_t kTile = kT * kHD * 2;  // 32 KB
+constexpr int kThreads = 384;
+constexpr float kRescaleLog2 = 8.f;       // lazy rescale threshold (p <= 2^8 between rescales)
+
+// K-major SWIZZLE_128B operand, K step t (16 elements) of a 128-wide tile.
+__device__ __forceinline__ uint64_t kdesc(uint32_t base, int t) {
+    return sdesc(base + (t >> 2) * (kTile / 2) + (t & 3) * 32, 16, 1024);
+}
+// The same tile read as the MN-major operand of its transpose: K step t = 16 stored rows.
+__device__ __forceinline__ uint64_t mndesc(uint32_t base, int t) { return sdesc(base + t * 2048, kTile / 2, 1024); }
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+    return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
+}
+
+// Row r's 64 keys of half `half` (32 packed bf16 pairs) into a K-major SWIZZLE_128B tile.
+__device__ __forceinline__ void sts_row_half(uint8_t* tile, int half, int r, const uint32_t (&w)[32]) {
+    uint8_t* rowp = tile + half * (kTile / 2) + r * 128;
+#pragma unroll
+    for (int k8 = 0; k8 < 8; ++k8)
+        *reinterpret_cast<uint4*>(rowp + ((k8 ^ (r & 7)) << 4)) = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
+}
+
+__device__ __forceinline__ void load_tile(uint32_t dst, const CUtensorMap* m, uint32_t bar, int row, int head, int b) {
+    tma_load_4d(dst, m, bar, 0, row, head, b);
+    tma_load_4d(dst + kTile / 2, m, bar, 64, row, head, b);
+}
+
+__device__ __forceinline__ void ld64(uint32_t taddr, float (&v)[64]) {
+    ld32(taddr, *reinterpret_cast<float(*)[32]>(v));
+    ld32(taddr + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+}
+
+struct FwdParams {
+    int s, nh, B, h;
+    float sl2;        // softmax scale * log2(e)
+    uint16_t* O;      // [B][s][h], head slice at head * hd
+    float* lse2;      // [B][nh][s]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const FwdParams A) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sQ = sm;
+    uint8_t* sK = sm + kTile;      // [2]
+    uint8_t* sV = sm + 3 * kTile;  // [2]
+    uint8_t* sP = sm + 5 * kTile;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kTile);
+    uint64_t* q_full = bar;
+    uint64_t* k_full = bar + 1;   // [2]
+    uint64_t* k_empty = bar + 3;  // [2]
+    uint64_t* v_full = bar + 5;   // [2]
+    uint64_t* v_empty = bar + 7;  // [2]
+    uint64_t* s_full = bar + 9;   // [2]
+    uint64_t* s_free = bar + 11;  // [2]
+    uint64_t* p_full = bar + 13;
+    uint64_t* p_free = bar + 14;
+    uint64_t* o_full = bar + 15;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 16);
+    float* xmax = reinterpret_cast<float*>(bar + 18);  // [2 parity][2 halves][128 rows]
+    float* xsum = xmax + 2 * 2 * 128;                  // [2 halves][128 rows]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nqt = A.s / kT;
+    const int qt = nqt - 1 - (int)blockIdx.x;
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int n = qt + 1;  // key tiles 0..qt
+
+    if (warp == 0 && lane == 0) {
+        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+        mbar_init(smem_u32(q_full), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&k_full[i]), 1);
+            mbar_init(smem_u32(&k_empty[i]), 1);
+            mbar_init(smem_u32(&v_full[i]), 1);
+            mbar_init(smem_u32(&v_empty[i]), 1);
+            mbar_init(smem_u32(&s_full[i]), 1);
+            mbar_init(smem_u32(&s_free[i]), 8);
+        }
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(p_free), 1);
+        mbar_init(smem_u32(o_full), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_holder;  // S[0] 0-127, S[1] 128-255, O 256-383
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            mbar_expect_tx(smem_u32(q_full), kTile);
+            load_tile(smem_u32(sQ), &tmQ, smem_u32(q_full), qt * kT, head, b);
+            for (int j = 0; j < n; ++j) {
+                const int st = j & 1;
+                const uint32_t ph = (j >> 1) & 1;
+                mbar_wait(smem_u32(&k_empty[st]), ph ^ 1);
+                mbar_expect_tx(smem_u32(&k_full[st]), kTile);
+                load_tile(smem_u32(sK + st * kTile), &tmK, smem_u32(&k_full[st]), j * kT, head, b);
+                mbar_wait(smem_u32(&v_empty[st]), ph ^ 1);
+                mbar_expect_tx(smem_u32(&v_full[st]), kTile);
+                load_tile(smem_u32(sV + st * kTile), &tmV, smem_u32(&v_full[st]), j * kT, head, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+            constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (K-major) x V (MN-major)
+            mbar_wait(smem_u32(q_full), 0);
+            auto issue_S = [&](int j) {
+                const int st = j & 1;
+                const uint32_t ph = (j >> 1) & 1;
+                mbar_wait(smem_u32(&k_full[st]), ph);
+                mbar_wait(smem_u32(&s_free[st]), ph ^ 1);
+                fence_after();
+                const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + st * 128, kdesc(qa, t), kdesc(ka, t), idS, t > 0);
+                commit(smem_u32(&s_full[st]));
+                commit(smem_u32(&k_empty[st]));
+            };
+            issue_S(0);
+            for (int j = 0; j < n; ++j) {
+                if (j + 1 < n) issue_S(j + 1);  // scores of j+1 overlap the softmax of j
+                const int st = j & 1;
+                mbar_wait(smem_u32(p_full), j & 1);
+                mbar_wait(smem_u32(&v_full[st]), (j >> 1) & 1);
+                fence_after();
+                const uint32_t pa = smem_u32(sP), va = smem_u32(sV + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 256, kdesc(pa, t), mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
+                commit(smem_u32(p_free));
+                commit(smem_u32(&v_empty[st]));
+            }
+            commit(smem_u32(o_full));
+        }
+    } else if (warp >= 4) {  // ===== online softmax / epilogue =====
+        const int half = (warp - 4) >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const int q = qt * kT + r;
+        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+        const int pair_bar = 1 + quarter;  // named barrier of warps (quarter, quarter + 4)
+        const float sl2 = A.sl2;
+        float m_used = -INFINITY, l = 0.f;
+        for (int j = 0; j < n; ++j) {
+            const int st = j & 1;
+            mbar_wait(smem_u32(&s_full[st]), (j >> 1) & 1);
+            fence_after();
+            float v[64];
+            ld64(tmem + lane_base + st * 128 + half * 64, v);
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s_free[st]));
+            if (j == qt) {  // diagonal tile: keys > q are masked
+                const int lim = q - j * kT - half * 64;
+#pragma unroll
+                for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
+            }
+            float cm = v[0];
+#pragma unroll
+            for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+            xmax[(st * 2 + half) * 128 + r] = cm;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            const float mt = fmaxf(cm, xmax[(st * 2 + (half ^ 1)) * 128 + r]);  // finite: key 0 <= q
+            float alpha = 1.f;
+            bool rescale = false;
+            if (m_used == -INFINITY) {
+                m_used = mt;
+            } else if ((mt - m_used) * sl2 > kRescaleLog2) {
+                alpha = ex2_approx((m_used - mt) * sl2);
+                l *= alpha;
+                m_used = mt;
+                rescale = true;
+            }
+            const float mb = m_used * sl2;
+            uint32_t w[32];
+            float add = 0.f;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+                const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
+                add += p0 + p1;
+                w[i] = pack_bf16x2_rn(p0, p1);
+            }
+            l += add;
+            if (j > 0) mbar_wait(smem_u32(p_free), (j - 1) & 1);  // P V of j-1 done: sP and O are ours
+            if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective: alpha = 1 elsewhere
+                fence_after();
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    float o[32];
+                    const uint32_t ta = tmem + lane_base + 256 + half * 64 + c * 32;
+                    ld32(ta, o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] *= alpha;
+                    st32(ta, o);
+                }
+            }
+            sts_row_half(sP, half, r, w);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+        }
+        xsum[half * 128 + r] = l;
+        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+        const float lt = l + xsum[(half ^ 1) * 128 + r];
+        const float inv = 1.f / lt;
+        if (half == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
+        mbar_wait(smem_u32(o_full), 0);
+        fence_after();
+        uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + half * 64;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+            float v[32];
+            ld32(tmem + lane_base + 256 + half * 64 + c * 32, v);
+            uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+            for (int k8 = 0; k8 < 4; ++k8)
+                op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
+                                    pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+struct BwdParams {
+    int s, nh, B, h;
+    float sl2, scale;
+    const float* lse2;  // [B][nh][s]
+    const float* D;     // [B][nh][s]
+    uint16_t* dS;       // [B][nh][s][s]
+    uint16_t* dqkv;     // [B][s][3h]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams A) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sK = sm;
+    uint8_t* sV = sm + kTile;
+    uint8_t* sQ = sm + 2 * kTile;   // [2]
+    uint8_t* sdO = sm + 4 * kTile;  // [2]
+    uint8_t* sPS = sm + 6 * kTile;  // P_i, then dS_i
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kTile);
+    uint64_t* kv_full = bar;
+    uint64_t* st_full = bar + 1;   // [2]
+    uint64_t* st_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* s_free = bar + 6;
+    uint64_t* dp_full = bar + 7;
+    uint64_t* dp_free = bar + 8;
+    uint64_t* p_full = bar + 9;
+    uint64_t* pv_done = bar + 10;
+    uint64_t* ds_full = bar + 11;
+    uint64_t* ps_free = bar + 12;
+    uint64_t* acc_full = bar + 13;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 14);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = A.s / kT;
+    const int kt = (int)blockIdx.x;  // 0 = most query tiles first
+    const int head = blockIdx.y, b = blockIdx.z;
+    const int nq = nt - kt;          // query tiles kt .. nt-1
+
+    if (warp == 0 && lane == 0) {
+        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmdO})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+        mbar_init(smem_u32(kv_full), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&st_full[i]), 1);
+            mbar_init(smem_u32(&st_empty[i]), 1);
+        }
+        mbar_init(smem_u32(s_full), 1);
+        mbar_init(smem_u32(s_free), 8);
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(dp_free), 8);
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(pv_done), 1);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(ps_free), 1);
+        mbar_init(smem_u32(acc_full), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_holder;  // S 0-127, dP 128-255, dV 256-383, dK 384-511
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            mbar_expect_tx(smem_u32(kv_full), 2 * kTile);
+            load_tile(smem_u32(sK), &tmK, smem_u32(kv_full), kt * kT, head, b);
+            load_tile(smem_u32(sV), &tmV, smem_u32(kv_full), kt * kT, head, b);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i & 1, qi = kt + i;
+                mbar_wait(smem_u32(&st_empty[st]), ((i >> 1) & 1) ^ 1);
+                const uint32_t fb = smem_u32(&st_full[st]);
+                mbar_expect_tx(fb, 2 * kTile);
+                load_tile(smem_u32(sQ + st * kTile), &tmQ, fb, qi * kT, head, b);
+                load_tile(smem_u32(sdO + st * kTile), &tmdO, fb, qi * kT, head, b);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t idSS = idesc_bf16(128, 128, 0, 0);   // X (K-major) x Y^T (K-major)
+            constexpr uint32_t idACC = idesc_bf16(128, 128, 1, 1);  // X^T (MN-major) x Y (MN-major)
+            mbar_wait(smem_u32(kv_full), 0);
+            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), psa = smem_u32(sPS);
+            auto issue_S_dP = [&](int i) {  // S_i = Q_i K^T, dP_i = dO_i V^T
+                const int st = i & 1;
+                mbar_wait(smem_u32(&st_full[st]), (i >> 1) & 1);
+                mbar_wait(smem_u32(s_free), (i & 1) ^ 1);
+                fence_after();
+                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem, kdesc(qa, t), kdesc(ka, t), idSS, t > 0);
+                commit(smem_u32(s_full));
+                mbar_wait(smem_u32(dp_free), (i & 1) ^ 1);
+                fence_after();
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 128, kdesc(da, t), kdesc(va, t), idSS, t > 0);
+                commit(smem_u32(dp_full));
+            };
+            issue_S_dP(0);
+            for (int i = 0; i < nq; ++i) {
+                const int st = i & 1;
+                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
+                mbar_wait(smem_u32(p_full), i & 1);
+                fence_after();
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 256, mndesc(psa, t), mndesc(da, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
+                commit(smem_u32(pv_done));
+                if (i + 1 < nq) issue_S_dP(i + 1);  // the next tile's scores overlap this tile's dS
+                mbar_wait(smem_u32(ds_full), i & 1);
+                fence_after();
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 384, mndesc(psa, t), mndesc(qa, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
+                commit(smem_u32(&st_empty[st]));
+                commit(smem_u32(ps_free));
+            }
+            commit(smem_u32(acc_full));
+        }
+    } else if (warp >= 4) {  // ===== P, dS; epilogue =====
+        const int half = (warp - 4) >> 2, quarter = warp & 3;  // keys [64 * half, 64 * half + 64)
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+        const float sl2 = A.sl2;
+        for (int i = 0; i < nq; ++i) {
+            const int qi = kt + i;
+            const int q = qi * kT + r;
+            const size_t row = ((size_t)b * A.nh + head) * A.s + q;
+            const float lse = A.lse2[row], Dq = A.D[row];
+            mbar_wait(smem_u32(s_full), i & 1);
+            fence_after();
+            uint32_t w[32];
+            {
+                float v[64];
+                ld64(tmem + lane_base + half * 64, v);
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(s_free));
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    w[k] = pack_bf16x2_rn(ex2_approx(fmaf(v[2 * k], sl2, -lse)), ex2_approx(fmaf(v[2 * k + 1], sl2, -lse)));
+            }
+            if (qi == kt) {  // diagonal tile: keys > q have P = 0
+                const int lim = q - kt * kT - half * 64;
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    w[k] &= (2 * k <= lim ? 0x0000ffffu : 0u) | (2 * k + 1 <= lim ? 0xffff0000u : 0u);
+            }
+            if (i > 0) mbar_wait(smem_u32(ps_free), (i - 1) & 1);  // dK MMA of i-1 has read dS
+            sts_row_half(sPS, half, r, w);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+            mbar_wait(smem_u32(dp_full), i & 1);
+            fence_after();
+            uint32_t o[32];
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                float v[32];
+                ld32(tmem + lane_base + 128 + half * 64 + c * 32, v);
+#pragma unroll
+                for (int k = 0; k < 16; ++k) {
+                    const uint32_t pw = w[c * 16 + k];
+                    const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
+                    o[c * 16 + k] = pack_bf16x2_rn(p0 * (v[2 * k] - Dq), p1 * (v[2 * k + 1] - Dq));
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(dp_free));
+            mbar_wait(smem_u32(pv_done), i & 1);  // dV MMA has read P
+            sts_row_half(sPS, half, r, o);
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(ds_full));
+            uint4* g = reinterpret_cast<uint4*>(A.dS + row * (size_t)A.s + kt * kT + half * 64);
+#pragma unroll
+            for (int k8 = 0; k8 < 8; ++k8) g[k8] = make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+        }
+        mbar_wait(smem_u32(acc_full), 0);
+        fence_after();
+        // thread r = key row of the tile: dV, dK (x scale) -> dqkv
+        uint16_t* base = A.dqkv + ((size_t)b * A.s + (size_t)kt * kT + r) * 3 * A.h + (size_t)head * kHD + half * 64;
+#pragma unroll 1
+        for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
+            uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
+            const float f = which == 0 ? 1.f : A.scale;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                float v[32];
+                ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
+                uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8)
+                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
+                                        pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// Head view {hd, s, nh, B} of a [B][s][ld] bf16 buffer (ld = 3h for qkv, h for dO), box 64 x 128.
+bool head_view(CUtensorMap* m, const uint16_t* base, int s, int nh, int B, long long ld) {
+    EncodeFn fn = encode();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)kHD, (cuuint64_t)s, (cuuint64_t)nh, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)kHD * 2, (cuuint64_t)s * ld * 2};
+    cuuint32_t box[4] = {64, 128, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes, bool& done) {
+    if (done) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) done = true;
+    return e;
+}
+
+}  // namespace
+
+bool flash_supported(int hd, int s) { return hd == kHD && s % kT == 0 && s >= kT; }
+
+cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
+                      cudaStream_t st) {
+    if (!flash_supported(hd, s)) return cudaErrorInvalidValue;
+    const int h = nh * hd;
+    CUtensorMap mq, mk, mv;
+    if (!head_view(&mq, qkv, s, nh, B, 3ll * h) || !head_view(&mk, qkv + h, s, nh, B, 3ll * h) ||
+        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h))
+        return cudaErrorInvalidValue;
+    FwdParams a;
+    a.s = s;
+    a.nh = nh;
+    a.B = B;
+    a.h = h;
+    a.sl2 = scale * 1.4426950408889634f;
+    a.O = O;
+    a.lse2 = lse2;
+    const size_t smem = 1024 + 6 * (size_t)kTile + 18 * 8 + 6 * 128 * 4;
+    static bool cfg = false;
+    cudaError_t e = set_smem(flash_fwd_kernel, smem, cfg);
+    if (e != cudaSuccess) return e;
+    flash_fwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, a);
+    return launched(1);
+}
+
+cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2, float* D,
+                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st) {
+    if (!flash_supported(hd, s)) return cudaErrorInvalidValue;
+    const int h = nh * hd;
+    cudaError_t e = attn_rowdot(dO, O, D, B, s, nh, st);
+    if (e != cudaSuccess) return e;
+    CUtensorMap mq, mk, mv, mdo;
+    if (!head_view(&mq, qkv, s, nh, B, 3ll * h) || !head_view(&mk, qkv + h, s, nh, B, 3ll * h) ||
+        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h) || !head_view(&mdo, dO, s, nh, B, h))
+        return cudaErrorInvalidValue;
+    BwdParams a;
+    a.s = s;
+    a.nh = nh;
+    a.B = B;
+    a.h = h;
+    a.sl2 = scale * 1.4426950408889634f;
+    a.scale = scale;
+    a.lse2 = lse2;
+    a.D = D;
+    a.dS = dS;
+    a.dqkv = dqkv;
+    const size_t smem = 1024 + 7 * (size_t)kTile + 16 * 8;
+    static bool cfg = false;
+    e = set_smem(flash_bwd_kernel, smem, cfg);
+    if (e != cudaSuccess) return e;
+    flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, a);
+    return launched(1);
+}
+
+}  // namespace gpt
+}  // namespace ah

@@ -165,33 +165,36 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         const uint32_t lane_base = uint32_t((warp & 3) * 32) << 16;
         const int q = qt * kBQ + r;
         float* red = reinterpret_cast<float*>(tmem_holder + 4);  // [2 halves][2 (m, l)][128 rows]
-        float m = -INFINITY, l = 0.f;
+        // Work in the log2 domain on raw scores: max over raw S (the scale is positive), then
+        // p = 2^(S * scale_log2 - m * scale_log2). Only the diagonal tile (j == qt) is masked.
+        const float sl2 = A.scale_log2;
+        float m = -INFINITY, l = 0.f;  // m: raw-score max of this half's keys
         for (int j = 0; j < n; ++j) {  // pass 1: exact row max and sum over this half's keys
             const int buf = j & 1, u = j >> 1;
             mbar_wait(smem_u32(&s_full[buf]), u & 1);
             fence_after();
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-                float v[32];
-                const int col0 = half * 64 + c * 32;
-                ld32(tmem + lane_base + buf * 128 + col0, v);
-                float cm = -INFINITY;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    v[i] = j * kBK + col0 + i <= q ? v[i] * A.scale_log2 : -INFINITY;
-                    cm = fmaxf(cm, v[i]);
-                }
-                if (cm == -INFINITY) continue;  // fully masked chunk
-                const float mn = fmaxf(m, cm);
-                float add = 0.f;
-#pragma unroll
-                for (int i = 0; i < 32; ++i) add += exp2f(v[i] - mn);
-                l = (m == -INFINITY ? 0.f : l * exp2f(m - mn)) + add;
-                m = mn;
-            }
+            float v[64];
+            ld32(tmem + lane_base + buf * 128 + half * 64, *reinterpret_cast<float(*)[32]>(v));
+            ld32(tmem + lane_base + buf * 128 + half * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&s_free[buf]));
+            if (lane == 0) mbar_arrive(smem_u32(&s_free[buf]));  // scores are in registers now
+            if (j == qt) {
+                const int lim = q - j * kBK - half * 64;  // keys <= q stay
+#pragma unroll
+                for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
+            }
+            float cm = v[0];
+#pragma unroll
+            for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+            if (cm == -INFINITY) continue;  // fully masked half row
+            const float mn = fmaxf(m, cm);
+            const float mb = mn * sl2;
+            float add = 0.f;
+#pragma unroll
+            for (int i = 0; i < 64; ++i) add += ex2_approx(fmaf(v[i], sl2, -mb));
+            l = (m == -INFINITY ? 0.f : l * ex2_approx((m - mn) * sl2)) + add;
+            m = mn;
         }
         red[(half * 2 + 0) * 128 + r] = m;
         red[(half * 2 + 1) * 128 + r] = l;
@@ -199,47 +202,46 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
         {
             const float mo = red[((half ^ 1) * 2 + 0) * 128 + r], lo = red[((half ^ 1) * 2 + 1) * 128 + r];
             const float mt = fmaxf(m, mo);
-            l = (m == -INFINITY ? 0.f : l * exp2f(m - mt)) + (mo == -INFINITY ? 0.f : lo * exp2f(mo - mt));
+            l = (m == -INFINITY ? 0.f : l * ex2_approx((m - mt) * sl2)) + (mo == -INFINITY ? 0.f : lo * ex2_approx((mo - mt) * sl2));
             m = mt;
         }
-        const float inv_l = 1.f / l;
+        // p = 2^(S * sl2 - (m * sl2 + log2 l)): normalisation folded into the exponent
+        const float off = fmaf(m, sl2, __log2f(l));
         uint16_t* prow = A.P + (((size_t)b * A.nh + head) * A.s + q) * (size_t)A.s;
         for (int j = 0; j < n; ++j) {  // pass 2: normalised P -> smem (A operand) + HBM
             const int g = n + j, buf = g & 1, u = g >> 1;
             mbar_wait(smem_u32(&s_full[buf]), u & 1);
             fence_after();
-            if (j > 0) mbar_wait(smem_u32(p_free), (j - 1) & 1);
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-                float v[32];
-                const int col0 = half * 64 + c * 32;
-                ld32(tmem + lane_base + buf * 128 + col0, v);
-                uint32_t w[16];
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int key = j * kBK + col0 + 2 * i;
-                    const float p0 = key <= q ? exp2f(v[2 * i] * A.scale_log2 - m) * inv_l : 0.f;
-                    const float p1 = key + 1 <= q ? exp2f(v[2 * i + 1] * A.scale_log2 - m) * inv_l : 0.f;
-                    w[i] = pack_bf16x2(p0, p1);
-                }
-                // smem: K-major SWIZZLE_128B tile; this half's 64 keys are atom `half`
-                uint8_t* rowp = sP + half * (kTile / 2) + r * 128;
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8) {
-                    const int chunk = (c * 4 + k8) ^ (r & 7);
-                    *reinterpret_cast<uint4*>(rowp + chunk * 16) = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
-                }
-                uint4* gp = reinterpret_cast<uint4*>(prow + j * kBK + col0);
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8) gp[k8] = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
-            }
+            float v[64];
+            ld32(tmem + lane_base + buf * 128 + half * 64, *reinterpret_cast<float(*)[32]>(v));
+            ld32(tmem + lane_base + buf * 128 + half * 64 + 32, *reinterpret_cast<float(*)[32]>(v + 32));
             fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&s_free[buf]));
+            uint32_t w[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                w[i] = pack_bf16x2_rn(ex2_approx(fmaf(v[2 * i], sl2, -off)), ex2_approx(fmaf(v[2 * i + 1], sl2, -off)));
+            if (j == qt) {  // causal mask of the diagonal tile: zero keys > q
+                const int lim = q - j * kBK - half * 64;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t keep = (2 * i <= lim ? 0x0000ffffu : 0u) | (2 * i + 1 <= lim ? 0xffff0000u : 0u);
+                    w[i] &= keep;
+                }
+            }
+            if (j > 0) mbar_wait(smem_u32(p_free), (j - 1) & 1);
+            // smem: K-major SWIZZLE_128B tile; this half's 64 keys are atom `half`
+            uint8_t* rowp = sP + half * (kTile / 2) + r * 128;
+#pragma unroll
+            for (int k8 = 0; k8 < 8; ++k8)
+                *reinterpret_cast<uint4*>(rowp + ((k8 ^ (r & 7)) << 4)) = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(smem_u32(&s_free[buf]));
-                mbar_arrive(smem_u32(p_full));
-            }
+            if (lane == 0) mbar_arrive(smem_u32(p_full));
+            uint4* gp = reinterpret_cast<uint4*>(prow + j * kBK + half * 64);
+#pragma unroll
+            for (int k8 = 0; k8 < 8; ++k8) gp[k8] = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
         }
         mbar_wait(smem_u32(o_full), 0);
         fence_after();
@@ -252,8 +254,8 @@ attn_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
             uint4* op = reinterpret_cast<uint4*>(orow + col0);
 #pragma unroll
             for (int k8 = 0; k8 < 4; ++k8)
-                op[k8] = make_uint4(pack_bf16x2(v[8 * k8], v[8 * k8 + 1]), pack_bf16x2(v[8 * k8 + 2], v[8 * k8 + 3]),
-                                    pack_bf16x2(v[8 * k8 + 4], v[8 * k8 + 5]), pack_bf16x2(v[8 * k8 + 6], v[8 * k8 + 7]));
+                op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8], v[8 * k8 + 1]), pack_bf16x2_rn(v[8 * k8 + 2], v[8 * k8 + 3]),
+                                    pack_bf16x2_rn(v[8 * k8 + 4], v[8 * k8 + 5]), pack_bf16x2_rn(v[8 * k8 + 6], v[8 * k8 + 7]));
         }
     }
     fence_before();

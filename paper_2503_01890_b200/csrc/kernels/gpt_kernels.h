@@ -36,6 +36,17 @@ cudaError_t attn_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int B, int s
 bool attn_bwd_supported(int hd, int s);
 cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const uint16_t* P, float* D,
                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
+// D[b][head][q] = rowsum(dO * O) over the head's 128 columns (hd = 128).
+cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st);
+// Flash attention (attn_flash.cu): single-pass online softmax forward that keeps only O and the
+// per-row log2-domain log-sum-exp lse2 = max * scale * log2(e) + log2(sum) ([B][nh][s] fp32);
+// the backward recomputes P = 2^(S * scale * log2(e) - lse2) from Q, K and lse2, and emits dS
+// [B, nh, s, s] (for the dQ = dS K GEMM) and dK (x scale), dV into dqkv. D: B*nh*s scratch.
+bool flash_supported(int hd, int s);
+cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
+                      cudaStream_t st);
+cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2, float* D,
+                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
 // Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.
 cudaError_t softmax_fwd2(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd2(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);

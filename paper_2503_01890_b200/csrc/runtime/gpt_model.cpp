@@ -72,15 +72,7 @@ GemmArgs linear_wgrad(const GptDims& d, const uint16_t* dY, int N, const uint16_
     return g;
 }
 
-// Fused tcgen05 attention forward when the shape allows it (head_dim 128, s % 128 == 0);
-// AH_ATTENTION=unfused selects the GEMM + softmax + GEMM path (A/B checks, other shapes).
-bool fused_attention(const GptDims& d) {
-    static const bool off = [] {
-        const char* e = std::getenv("AH_ATTENTION");
-        return e && std::string(e) == "unfused";
-    }();
-    return !off && gpt::attn_fwd_supported(d.hd, d.s);
-}
+bool fused_attention(const GptDims& d) { return attention_mode(d) != AttnMode::Unfused; }
 
 // Per-(head, sequence) view helpers: z1 = head, z2 = sequence.
 void heads(GemmArgs& g, const GptDims& d) {
@@ -90,12 +82,31 @@ void heads(GemmArgs& g, const GptDims& d) {
 
 }  // namespace
 
+// head_dim 128 and s % 128 == 0 run a fused tcgen05 kernel; AH_ATTENTION=twopass / unfused
+// select the P-saving paths (A/B checks); other shapes fall back to unfused.
+AttnMode attention_mode(const GptDims& d) {
+    static const std::string env = [] {
+        const char* e = std::getenv("AH_ATTENTION");
+        return std::string(e ? e : "");
+    }();
+    if (env == "unfused" || !gpt::flash_supported(d.hd, d.s)) return AttnMode::Unfused;
+    if (env == "twopass" || env == "fused") return AttnMode::TwoPass;
+    return AttnMode::Flash;
+}
+
+namespace {
+size_t saved_probs_bytes(const GptDims& d) {  // P (bf16, s x s per head) or lse2 (fp32 per row)
+    const size_t rows = (size_t)d.B * d.nh * d.s;
+    return attention_mode(d) == AttnMode::Flash ? rows * 4 : rows * d.s * 2;
+}
+}  // namespace
+
 size_t BlockActs::bytes(const GptDims& d) {
     const size_t T = d.T(), h = d.h;
     size_t b = 0;
     b += align_up(T * h * 2);                        // ln1
     b += align_up(T * 3 * h * 2);                    // qkv
-    b += align_up((size_t)d.B * d.nh * d.s * d.s * 2);  // P
+    b += align_up(saved_probs_bytes(d));             // P or lse2
     b += align_up(T * h * 2);                        // att
     b += align_up(T * h * 2);                        // x2
     b += align_up(T * h * 2);                        // ln2
@@ -115,7 +126,15 @@ BlockActs BlockActs::carve(const GptDims& d, void* base) {
     BlockActs a;
     a.ln1 = reinterpret_cast<uint16_t*>(take(T * h * 2));
     a.qkv = reinterpret_cast<uint16_t*>(take(T * 3 * h * 2));
-    a.P = reinterpret_cast<uint16_t*>(take((size_t)d.B * d.nh * d.s * d.s * 2));
+    {
+        uint8_t* pr = take(saved_probs_bytes(d));
+        if (attention_mode(d) == AttnMode::Flash) {
+            a.P = nullptr;
+            a.lse2 = reinterpret_cast<float*>(pr);
+        } else {
+            a.P = reinterpret_cast<uint16_t*>(pr);
+        }
+    }
     a.att = reinterpret_cast<uint16_t*>(take(T * h * 2));
     a.x2 = reinterpret_cast<uint16_t*>(take(T * h * 2));
     a.ln2 = reinterpret_cast<uint16_t*>(take(T * h * 2));
@@ -128,10 +147,17 @@ BlockActs BlockActs::carve(const GptDims& d, void* base) {
     return a;
 }
 
+namespace {
+size_t ws_s_bytes(const GptDims& d) {  // fp32 scores (unfused) or the row dot D (fused)
+    const size_t rows = (size_t)d.B * d.nh * d.s;
+    return attention_mode(d) == AttnMode::Unfused ? rows * d.s * 4 : rows * 4;
+}
+}  // namespace
+
 size_t Workspace::bytes(const GptDims& d) {
     const size_t T = d.T(), h = d.h, Z = (size_t)d.B * d.nh;
     const size_t part_rows = (size_t)std::max(gpt::ln_bwd_ctas(d.T()), gpt::colsum_rows(d.T()));
-    return align_up(Z * d.s * d.s * 4) + align_up(Z * d.s * d.s * 2) + align_up(T * 4 * h * 2) +
+    return align_up(ws_s_bytes(d)) + align_up(Z * d.s * d.s * 2) + align_up(T * 4 * h * 2) +
            align_up(T * 3 * h * 2) + 3 * align_up(T * h * 2) + align_up(part_rows * 4 * h * 4);
 }
 
@@ -145,7 +171,7 @@ Workspace Workspace::carve(const GptDims& d, void* base) {
         return r;
     };
     Workspace w;
-    w.S = reinterpret_cast<float*>(take(Z * d.s * d.s * 4));
+    w.S = reinterpret_cast<float*>(take(ws_s_bytes(d)));
     w.dS = reinterpret_cast<uint16_t*>(take(Z * d.s * d.s * 2));
     w.d4h = reinterpret_cast<uint16_t*>(take(T * 4 * h * 2));
     w.dqkv = reinterpret_cast<uint16_t*>(take(T * 3 * h * 2));
@@ -167,7 +193,10 @@ cudaError_t block_forward(const GptDims& d, const uint16_t* W, const uint16_t* x
         g.bias = W + o.b_qkv;
         AH_TRY(gemm::run(g, st));
     }
-    if (fused_attention(d)) {  // one tcgen05 kernel: S, softmax, P (kept for the backward), P V
+    const AttnMode mode = attention_mode(d);
+    if (mode == AttnMode::Flash) {  // one tcgen05 kernel: S, online softmax, P V; keeps O and lse
+        AH_TRY(gpt::flash_fwd(a.qkv, a.att, a.lse2, d.B, s, d.nh, hd, 1.0f / std::sqrt((float)hd), st));
+    } else if (mode == AttnMode::TwoPass) {  // S, exact softmax, P (kept for the backward), P V
         AH_TRY(gpt::attn_fwd(a.qkv, a.P, a.att, d.B, s, d.nh, hd, 1.0f / std::sqrt((float)hd), st));
     } else {
     {  // S = Q K^T / sqrt(hd), causal tiles only, fp32
@@ -249,7 +278,9 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
     AH_TRY(gpt::colsum(ws.dx2, T, h, h, ws.part, W + o.b_proj, 0, st));
     // ---- attention core, per (head, sequence)
     const bool fused = fused_attention(d);
-    if (fused) {  // one tcgen05 kernel: dP, dS (-> HBM for dQ), dV, dK; D = rowsum(dO * O) in ws.S
+    if (attention_mode(d) == AttnMode::Flash) {  // P recomputed from lse; dS (-> HBM for dQ), dV, dK
+        AH_TRY(gpt::flash_bwd(a.qkv, a.att, ws.datt, a.lse2, ws.S, ws.dS, ws.dqkv, d.B, s, d.nh, hd, scale, st));
+    } else if (fused) {  // one tcgen05 kernel: dP, dS (-> HBM for dQ), dV, dK; D = rowsum(dO * O) in ws.S
         AH_TRY(gpt::attn_bwd(a.qkv, a.att, ws.datt, a.P, ws.S, ws.dS, ws.dqkv, d.B, s, d.nh, hd, scale, st));
     } else {
     {  // dP = dO V^T (fp32, lower tiles)

@@ -42,8 +42,15 @@ struct BlockLayout {
 
 // Saved activations of one block besides its input (the recomputable "drop" part of
 // simulator.cpp:98-102): carved from one allocation.
+// Attention implementation (process-wide, env AH_ATTENTION): flash (default: O + per-row lse
+// saved, P recomputed in the backward), twopass (fused two-pass kernel, P saved) or unfused
+// (GEMM + softmax + GEMM, P saved). It decides what a block keeps (P or lse) and the workspace.
+enum class AttnMode { Flash, TwoPass, Unfused };
+AttnMode attention_mode(const GptDims& d);
+
 struct BlockActs {
-    uint16_t *ln1, *qkv, *P, *att, *x2, *ln2, *fc_pre, *gelu;
+    uint16_t *ln1, *qkv, *P, *att, *x2, *ln2, *fc_pre, *gelu;  // P: [B*nh, s, s] (not in flash mode)
+    float* lse2 = nullptr;                                      // flash: [B*nh, s] log2-domain lse
     float *mean1, *rstd1, *mean2, *rstd2;
     static size_t bytes(const GptDims& d);
     static BlockActs carve(const GptDims& d, void* base);
@@ -51,7 +58,7 @@ struct BlockActs {
 
 // Transient per-step scratch shared by all blocks (part of the constant residue m_gc).
 struct Workspace {
-    float* S = nullptr;        // [B*nh, s, s] fp32 scores / dP
+    float* S = nullptr;        // unfused: [B*nh, s, s] fp32 scores / dP; fused: D = rowsum(dO*O) [B*nh, s]
     uint16_t* dS = nullptr;    // [B*nh, s, s]
     uint16_t* d4h = nullptr;   // [T, 4h]
     uint16_t* dqkv = nullptr;  // [T, 3h]

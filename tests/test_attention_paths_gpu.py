@@ -1,6 +1,6 @@
-"""The fused tcgen05 attention (forward + backward kernels) and the unfused GEMM + softmax +
-GEMM path give the same training step within bf16 tolerance (the unfused path is selected
-with AH_ATTENTION=unfused in a subprocess, since the choice is latched per process)."""
+"""The fused tcgen05 attention paths (flash: O + lse saved, P recomputed; twopass: P saved) and
+the unfused GEMM + softmax + GEMM path give the same training step within bf16 tolerance (the
+path is selected with AH_ATTENTION in a subprocess, since the choice is latched per process)."""
 import json
 import os
 import subprocess
@@ -36,8 +36,9 @@ def run(env_extra):
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
-def test_fused_and_unfused_attention_agree(cuda_device, native):
-    fused = run({})
+@pytest.mark.parametrize("mode", ["flash", "twopass"])
+def test_fused_and_unfused_attention_agree(cuda_device, native, mode):
+    fused = run({"AH_ATTENTION": mode})
     unfused = run({"AH_ATTENTION": "unfused"})
     assert abs(fused["loss"] - unfused["loss"]) < 1e-3 * abs(unfused["loss"])
     for a, b in zip(fused["delta"], unfused["delta"]):

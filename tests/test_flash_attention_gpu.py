@@ -1,0 +1,60 @@
+"""Flash attention (online-softmax forward keeping O + lse, P-recomputing backward) against a
+torch fp32 reference of causal softmax(Q K^T / sqrt(d)) V and its autograd gradients.
+Tolerances: bf16 operands, bf16 P / dS, fp32 accumulation (relative Frobenius error)."""
+import math
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def reference(qkv, nh):
+    B, s, h3 = qkv.shape
+    h, hd = h3 // 3, h3 // 3 // nh
+    x = qkv.float().detach().requires_grad_(True)
+    q, k, v = (t.view(B, s, nh, hd).transpose(1, 2) for t in x.split(h, dim=-1))
+    S = q @ k.transpose(-1, -2) / math.sqrt(hd)
+    mask = torch.ones(s, s, device=qkv.device).tril().bool()
+    S = S.masked_fill(~mask, float("-inf"))
+    lse2 = torch.logsumexp(S, dim=-1) / math.log(2.0)
+    O = (torch.softmax(S, dim=-1) @ v).transpose(1, 2).reshape(B, s, h)
+    return x, O, lse2
+
+
+def rel(a, b):
+    return float((a.detach().float() - b.detach().float()).norm() / b.detach().float().norm())
+
+
+@pytest.mark.parametrize("B,s,nh,amp", [(1, 128, 1, 0.5), (2, 256, 2, 0.5), (2, 1024, 4, 0.5), (1, 512, 2, 4.0)])
+def test_flash_forward_and_backward(cuda_device, native, B, s, nh, amp):
+    """amp 4.0 gives large score ranges, exercising the lazy O / l rescale."""
+    from paper_2503_01890_b200.attention import flash_bwd, flash_fwd
+    hd = 128
+    g = torch.Generator(device="cuda").manual_seed(7 * s + nh)
+    qkv = (torch.randn(B, s, 3 * nh * hd, device="cuda", generator=g) * amp).bfloat16()
+    O, lse2 = flash_fwd(qkv, nh)
+    x, Or, lr = reference(qkv, nh)
+    assert rel(O, Or) < 1e-2
+    assert (lse2 - lr).abs().max() < 2e-3 * max(1.0, float(lr.abs().max()))
+    dO = torch.randn(B, s, nh * hd, device="cuda", generator=g).bfloat16()
+    dqkv = flash_bwd(qkv, O, dO, lse2, nh)
+    torch.cuda.synchronize()
+    Or.backward(dO.float())
+    ref = x.grad
+    h = nh * hd
+    for i, name in enumerate(("dQ", "dK", "dV")):
+        err = rel(dqkv[..., i * h:(i + 1) * h], ref[..., i * h:(i + 1) * h])
+        assert err < 2e-2, (name, err)
+
+
+def test_flash_is_deterministic(cuda_device, native):
+    from paper_2503_01890_b200.attention import flash_bwd, flash_fwd
+    qkv = (torch.randn(2, 512, 3 * 256, device="cuda") * 0.5).bfloat16()
+    dO = torch.randn(2, 512, 256, device="cuda").bfloat16()
+    O1, l1 = flash_fwd(qkv, 2)
+    O2, l2 = flash_fwd(qkv, 2)
+    d1 = flash_bwd(qkv, O1, dO, l1, 2)
+    d2 = flash_bwd(qkv, O2, dO, l2, 2)
+    torch.cuda.synchronize()
+    assert torch.equal(O1, O2) and torch.equal(l1, l2) and torch.equal(d1, d2)
