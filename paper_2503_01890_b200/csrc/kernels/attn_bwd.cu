@@ -229,25 +229,31 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
     }
 }
 
-// D[b][head][q] = sum_c dO[b, q, head*hd + c] * O[b, q, head*hd + c]; one warp per (b, q, head).
+// D[b][head][q] = sum_c dO[b, q, head*hd + c] * O[b, q, head*hd + c]. Half a warp per
+// (b, q, head) row: 16 lanes x 16-byte loads cover the 128 head columns; grid-stride.
 __global__ void attn_bwd_dot_kernel(const uint16_t* __restrict__ dO, const uint16_t* __restrict__ O, float* __restrict__ D,
                                     int B, int s, int nh) {
-    const long long w = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (w >= (long long)B * s * nh) return;
-    const int head = (int)(w % nh);
-    const long long bq = w / nh;  // b * s + q
-    const size_t off = (size_t)bq * nh * kHD + (size_t)head * kHD + lane * 4;
-    const uint2 a = *reinterpret_cast<const uint2*>(dO + off);
-    const uint2 o = *reinterpret_cast<const uint2*>(O + off);
-    float t = bf16_bits_to_f32(a.x & 0xffffu) * bf16_bits_to_f32(o.x & 0xffffu) +
-              bf16_bits_to_f32(a.x >> 16) * bf16_bits_to_f32(o.x >> 16) +
-              bf16_bits_to_f32(a.y & 0xffffu) * bf16_bits_to_f32(o.y & 0xffffu) +
-              bf16_bits_to_f32(a.y >> 16) * bf16_bits_to_f32(o.y >> 16);
-    t = warp_sum(t);
-    if (lane == 0) {
-        const long long bb = bq / s, q = bq % s;
-        D[(bb * nh + head) * s + q] = t;
+    const long long rows = (long long)B * s * nh;
+    const int sub = threadIdx.x & 15;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; w < rows;
+         w += ((long long)gridDim.x * blockDim.x) >> 4) {
+        const size_t off = (size_t)w * kHD + sub * 8;  // (b*s + q)*h + head*hd == w*hd
+        const uint4 a = *reinterpret_cast<const uint4*>(dO + off);
+        const uint4 o = *reinterpret_cast<const uint4*>(O + off);
+        const uint32_t au[4] = {a.x, a.y, a.z, a.w}, ou[4] = {o.x, o.y, o.z, o.w};
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            t += bf16_bits_to_f32(au[k] & 0xffffu) * bf16_bits_to_f32(ou[k] & 0xffffu) +
+                 bf16_bits_to_f32(au[k] >> 16) * bf16_bits_to_f32(ou[k] >> 16);
+#pragma unroll
+        for (int o2 = 8; o2 > 0; o2 >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o2);
+        if (sub == 0) {
+            const int head = (int)(w % nh);
+            const long long bq = w / nh;  // b * s + q
+            const long long bb = bq / s, q = bq % s;
+            D[(bb * nh + head) * s + q] = t;
+        }
     }
 }
 
@@ -285,7 +291,7 @@ bool map4(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint
 bool attn_bwd_supported(int hd, int s) { return hd == kHD && s % kT == 0; }
 
 cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st) {
-    attn_bwd_dot_kernel<<<(unsigned)(((long long)B * s * nh + 7) / 8), 256, 0, st>>>(dO, O, D, B, s, nh);
+    attn_bwd_dot_kernel<<<kNumSMs * 8, 256, 0, st>>>(dO, O, D, B, s, nh);
     return launched(1);
 }
 
@@ -293,7 +299,7 @@ cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO,
                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st) {
     if (!attn_bwd_supported(hd, s)) return cudaErrorInvalidValue;
     const int h = nh * hd;
-    attn_bwd_dot_kernel<<<(unsigned)(((long long)B * s * nh + 7) / 8), 256, 0, st>>>(dO, O, D, B, s, nh);
+    attn_bwd_dot_kernel<<<kNumSMs * 8, 256, 0, st>>>(dO, O, D, B, s, nh);
     launched(1);
     CUtensorMap mq, mv, mdo, mp;
     const cuuint64_t row3 = 3ull * h;

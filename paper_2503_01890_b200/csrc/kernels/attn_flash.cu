@@ -288,7 +288,8 @@ struct BwdParams {
 
 __global__ void __launch_bounds__(kThreads, 1)
 flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO, const BwdParams A) {
+                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                 const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
     uint8_t* sK = sm;
@@ -406,11 +407,18 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = uint32_t(quarter * 32) << 16;
         const float sl2 = A.sl2;
+        const size_t row0 = ((size_t)b * A.nh + head) * A.s + (size_t)kt * kT + r;
+        float lse_n = A.lse2[row0], D_n = A.D[row0];  // row statistics, prefetched one tile ahead
+        uint8_t* slab = sPS + half * (kTile / 2) + quarter * 4096;  // this warp's 32 rows x 64 keys
         for (int i = 0; i < nq; ++i) {
             const int qi = kt + i;
             const int q = qi * kT + r;
-            const size_t row = ((size_t)b * A.nh + head) * A.s + q;
-            const float lse = A.lse2[row], Dq = A.D[row];
+            const size_t row = row0 + (size_t)i * kT;
+            const float lse = lse_n, Dq = D_n;
+            if (i + 1 < nq) {
+                lse_n = A.lse2[row + kT];
+                D_n = A.D[row + kT];
+            }
             mbar_wait(smem_u32(s_full), i & 1);
             fence_after();
             uint32_t w[32];
@@ -430,7 +438,11 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
                 for (int k = 0; k < 32; ++k)
                     w[k] &= (2 * k <= lim ? 0x0000ffffu : 0u) | (2 * k + 1 <= lim ? 0xffff0000u : 0u);
             }
-            if (i > 0) mbar_wait(smem_u32(ps_free), (i - 1) & 1);  // dK MMA of i-1 has read dS
+            if (i > 0) {
+                mbar_wait(smem_u32(ps_free), (i - 1) & 1);  // dK MMA of i-1 has read dS
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // and the dS store
+                __syncwarp();
+            }
             sts_row_half(sPS, half, r, w);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
@@ -456,11 +468,18 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             sts_row_half(sPS, half, r, o);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(ds_full));
-            uint4* g = reinterpret_cast<uint4*>(A.dS + row * (size_t)A.s + kt * kT + half * 64);
-#pragma unroll
-            for (int k8 = 0; k8 < 8; ++k8) g[k8] = make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+            if (lane == 0) {
+                mbar_arrive(smem_u32(ds_full));
+                // this warp's 32 x 64 dS slab -> HBM (the smem slab is the box's SWIZZLE_128B image)
+                asm volatile(
+                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                        reinterpret_cast<uint64_t>(&tmdS)),
+                    "r"(smem_u32(slab)), "r"(kt * kT + half * 64), "r"(qi * kT + quarter * 32), "r"(head), "r"(b)
+                    : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         mbar_wait(smem_u32(acc_full), 0);
         fence_after();
         // thread r = key row of the tile: dV, dK (x scale) -> dqkv
@@ -518,6 +537,18 @@ bool head_view(CUtensorMap* m, const uint16_t* base, int s, int nh, int B, long 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// [B][nh][s][s] bf16 probabilities-shaped buffer (dS), box 64 keys x 32 query rows (store slabs).
+bool probs_view(CUtensorMap* m, uint16_t* base, int s, int nh, int B) {
+    EncodeFn fn = encode();
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)s, (cuuint64_t)s, (cuuint64_t)nh, (cuuint64_t)B};
+    cuuint64_t strides[3] = {(cuuint64_t)s * 2, (cuuint64_t)s * s * 2, (cuuint64_t)nh * s * s * 2};
+    cuuint32_t box[4] = {64, 32, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <typename K>
 cudaError_t set_smem(K kernel, size_t bytes, bool& done) {
     if (done) return cudaSuccess;
@@ -560,9 +591,10 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     const int h = nh * hd;
     cudaError_t e = attn_rowdot(dO, O, D, B, s, nh, st);
     if (e != cudaSuccess) return e;
-    CUtensorMap mq, mk, mv, mdo;
+    CUtensorMap mq, mk, mv, mdo, mds;
     if (!head_view(&mq, qkv, s, nh, B, 3ll * h) || !head_view(&mk, qkv + h, s, nh, B, 3ll * h) ||
-        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h) || !head_view(&mdo, dO, s, nh, B, h))
+        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h) || !head_view(&mdo, dO, s, nh, B, h) ||
+        !probs_view(&mds, dS, s, nh, B))
         return cudaErrorInvalidValue;
     BwdParams a;
     a.s = s;
@@ -579,7 +611,7 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     static bool cfg = false;
     e = set_smem(flash_bwd_kernel, smem, cfg);
     if (e != cudaSuccess) return e;
-    flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, a);
+    flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
     return launched(1);
 }
 
