@@ -165,6 +165,47 @@ __global__ void colsum_partial_kernel(const uint16_t* __restrict__ X, int T, int
     for (int i = 0; i < 8; ++i) dst[i] = a[i];
 }
 
+// part[r][n] = sum over rows [r*rows, min(T, (r+1)*rows)) of X[row][n]. CTA = 32 column
+// groups (8 columns, 16-byte loads) x 8 row lanes with four loads in flight per thread; the
+// row lanes are combined in smem in a fixed order (deterministic).
+__global__ void __launch_bounds__(256) colsum_partial2_kernel(const uint16_t* __restrict__ X, int T, int N, int ldx,
+                                                              int rows, float* __restrict__ part) {
+    __shared__ float red[8][256];
+    const int cg = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int c = (blockIdx.x * 32 + cg) * 8;
+    const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+    float a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (c < N) {
+        int r = r0 + ry;
+        for (; r + 24 < r1; r += 32) {
+            uint4 w[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) w[u] = ldg16(X + (size_t)(r + 8 * u) * ldx + c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                float f[8];
+                unpack8(w[u], f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) a[i] += f[i];
+            }
+        }
+        for (; r < r1; r += 8) {
+            float f[8];
+            unpack8(ldg16(X + (size_t)r * ldx + c), f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] += f[i];
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) red[ry][i * 32 + cg] = a[i];
+    __syncthreads();
+    const int t = threadIdx.x, n = blockIdx.x * 256 + t;
+    float sum = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) sum += red[q][(t & 7) * 32 + (t >> 3)];
+    if (n < N) part[(size_t)blockIdx.y * N + n] = sum;
+}
+
 // out[n] (bf16 or fp32) = sum_r part[r][n], r ascending.
 __global__ void colsum_finish_kernel(const float* __restrict__ part, int R, int N, void* out, int out_f32,
                                      float* out2_f32) {
@@ -455,13 +496,15 @@ cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, con
     return launched(2);
 }
 
-int colsum_rows(int T) { return T >= 4096 ? 256 : (T >= 256 ? 32 : 1); }
+int colsum_rows(int T) { return T >= 4096 ? 64 : (T >= 256 ? 32 : 1); }
 
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st) {
     const int R = colsum_rows(T);
     const int rows = (T + R - 1) / R;
-    dim3 grid((N / 8 + 127) / 128, R);
-    colsum_partial_kernel<<<grid, 128, 0, st>>>(X, T, N, ldx, rows, part);
+    if (N % 8 == 0 && ldx % 8 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0)
+        colsum_partial2_kernel<<<dim3((N + 255) / 256, R), 256, 0, st>>>(X, T, N, ldx, rows, part);
+    else
+        colsum_partial_kernel<<<dim3((N / 8 + 127) / 128, R), 128, 0, st>>>(X, T, N, ldx, rows, part);
     launched(1);
     return colsum_finish_wide(part, R, N, out, out_f32, st);
 }
@@ -709,15 +752,79 @@ __global__ void ln_bwd_dgdb_kernel(const uint16_t* __restrict__ dy, const uint16
         dst[h + c + i] = db[i];
     }
 }
+// Same reduction with the colsum_partial2 layout: 32 column groups x 8 row lanes per CTA.
+__global__ void __launch_bounds__(256) ln_bwd_dgdb2_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                                                           const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                           int T, int h, int rows, float* __restrict__ part) {
+    __shared__ float red[8][2][256];
+    const int cg = threadIdx.x & 31, ry = threadIdx.x >> 5;
+    const int c = (blockIdx.x * 32 + cg) * 8;
+    const int r0 = blockIdx.y * rows, r1 = min(T, r0 + rows);
+    float dg[8] = {0, 0, 0, 0, 0, 0, 0, 0}, db[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (c < h) {
+        int r = r0 + ry;
+        for (; r + 8 < r1; r += 16) {
+            const uint4 x0 = ldg16(x + (size_t)r * h + c), d0 = ldg16(dy + (size_t)r * h + c);
+            const uint4 x1 = ldg16(x + (size_t)(r + 8) * h + c), d1 = ldg16(dy + (size_t)(r + 8) * h + c);
+            const float mu0 = mean[r], rs0 = rstd[r], mu1 = mean[r + 8], rs1 = rstd[r + 8];
+            float xf[8], df[8];
+            unpack8(x0, xf);
+            unpack8(d0, df);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                dg[i] += df[i] * (xf[i] - mu0) * rs0;
+                db[i] += df[i];
+            }
+            unpack8(x1, xf);
+            unpack8(d1, df);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                dg[i] += df[i] * (xf[i] - mu1) * rs1;
+                db[i] += df[i];
+            }
+        }
+        for (; r < r1; r += 8) {
+            float xf[8], df[8];
+            unpack8(ldg16(x + (size_t)r * h + c), xf);
+            unpack8(ldg16(dy + (size_t)r * h + c), df);
+            const float mu = mean[r], rs = rstd[r];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                dg[i] += df[i] * (xf[i] - mu) * rs;
+                db[i] += df[i];
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        red[ry][0][i * 32 + cg] = dg[i];
+        red[ry][1][i * 32 + cg] = db[i];
+    }
+    __syncthreads();
+    const int t = threadIdx.x, n = blockIdx.x * 256 + t;
+    float sg = 0.f, sb = 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        sg += red[q][0][(t & 7) * 32 + (t >> 3)];
+        sb += red[q][1][(t & 7) * 32 + (t >> 3)];
+    }
+    if (n < h) {
+        part[(size_t)blockIdx.y * 2 * h + n] = sg;
+        part[(size_t)blockIdx.y * 2 * h + h + n] = sb;
+    }
+}
 }  // namespace
 
-int reduce_chunks(int T) { return T >= 4096 ? 256 : (T >= 512 ? 32 : 1); }
+int reduce_chunks(int T) { return T >= 4096 ? 64 : (T >= 512 ? 32 : 1); }
 
 cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
                     const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st) {
     ln_bwd_dx_kernel<<<(T + 7) / 8, 256, 0, st>>>(dy, x, mean, rstd, g, dres, dx, T, h);
     const int R = reduce_chunks(T), rows = (T + R - 1) / R;
-    ln_bwd_dgdb_kernel<<<dim3((h / 8 + 127) / 128, R), 128, 0, st>>>(dy, x, mean, rstd, T, h, rows, part);
+    if (h % 8 == 0)
+        ln_bwd_dgdb2_kernel<<<dim3((h + 255) / 256, R), 256, 0, st>>>(dy, x, mean, rstd, T, h, rows, part);
+    else
+        ln_bwd_dgdb_kernel<<<dim3((h / 8 + 127) / 128, R), 128, 0, st>>>(dy, x, mean, rstd, T, h, rows, part);
     launched(2);
     return colsum_finish_wide(part, R, 2 * h, dgdb, 0, st);
 }
