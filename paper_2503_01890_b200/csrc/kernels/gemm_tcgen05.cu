@@ -223,17 +223,17 @@ __device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int cran
 
 // ---- work assignment -------------------------------------------------------------------
 // Data-parallel: cluster tiles strided over the grid (L2-friendly: concurrently running CTAs
-// share A panels). Tail split (P.sk, CS == 1): the W full waves stay data-parallel and each of
-// the remaining `tail` tiles (2 * tail <= grid) is split in two K halves on CTAs 2u (prefix,
-// processed FIRST, partial -> workspace slot + release flag) and 2u + 1 (suffix, processed
-// LAST, adds the partial before its epilogue), so the last wave costs half a tile instead of
-// a whole one (512 tiles on 148 SMs: 3.5 instead of 4 tile times).
+// share A panels). Tail split (P.sk): the W full waves stay data-parallel and each of the
+// remaining `tail` cluster tiles (2 * tail <= clusters) is split in two K halves on clusters
+// 2u (prefix, processed FIRST, partial -> workspace slot + release flag per CTA) and 2u + 1
+// (suffix, processed LAST, adds the partial before its epilogue), so the last wave costs half a
+// tile instead of a whole one (512 tiles on 148 SMs: 3.5 instead of 4 tile times).
 template <int CS>
 __device__ __forceinline__ int num_segments(const Params& P) {
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
     if (!P.sk) return cid < P.num_tiles ? (P.num_tiles - 1 - cid) / ncl + 1 : 0;
-    const int G = gridDim.x, waves = P.num_tiles / G, tail = P.num_tiles - waves * G;
-    return waves + ((int)blockIdx.x < 2 * tail ? 1 : 0);
+    const int waves = P.num_tiles / ncl, tail = P.num_tiles - waves * ncl;
+    return waves + (cid < 2 * tail ? 1 : 0);
 }
 
 template <int CS>
@@ -243,7 +243,7 @@ __device__ __forceinline__ Tile segment(const Params& P, int i, int BN, int cran
         T.role = 0;
         return T;
     }
-    const int G = gridDim.x, c = blockIdx.x, waves = P.num_tiles / G, tail = P.num_tiles - waves * G;
+    const int G = gridDim.x / CS, c = blockIdx.x / CS, waves = P.num_tiles / G, tail = P.num_tiles - waves * G;
     const bool unit = c < 2 * tail;
     const bool prefix = unit && (c & 1) == 0;
     int t, k0 = 0, k1 = P.k_blocks, role = 0;
@@ -254,7 +254,7 @@ __device__ __forceinline__ Tile segment(const Params& P, int i, int BN, int cran
     } else {
         t = c + (i - (prefix ? 1 : 0)) * G;
     }
-    Tile T = decode<1>(P, t, BN, 0);
+    Tile T = decode<CS>(P, t, BN, crank);
     T.kb0 = k0;
     T.kb1 = k1;
     T.role = role;
@@ -508,7 +508,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 if (warp == 0 && lane == 0) {
                     unsigned f = 0;
                     do {
-                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + blockIdx.x - 1) : "memory");
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(P.sk_flags + blockIdx.x - CS) : "memory");
                         if (f != P.sk_epoch) __nanosleep(64);
                     } while (f != P.sk_epoch);
                 }
@@ -526,7 +526,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const int n0 = T.tn * BN + c * 32;
                 if (rows <= 0 || n0 >= P.N) continue;  // warp-uniform
                 if (T.role != 0) {  // stream-K: raw fp32 accumulator row chunk <-> workspace slot
-                    const unsigned slot_cta = T.role == 1 ? blockIdx.x : blockIdx.x - 1;
+                    const unsigned slot_cta = T.role == 1 ? blockIdx.x : blockIdx.x - CS;  // same rank, previous cluster
                     float4* s4 = reinterpret_cast<float4*>(P.sk_ws + ((size_t)slot_cta * BM + q * 32 + lane) * BN + c * 32);
                     if (T.role == 1) {
 #pragma unroll
@@ -1082,12 +1082,15 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         const char* e = std::getenv("AH_GEMM_STREAMK");
         return e && std::string(e) == "0";
     }();
+    const int CS = (!no_cluster && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
+    if (CS > 1) P.num_tiles = ((P.tiles_m + CS - 1) / CS) * P.tiles_n * P.batch1 * P.batch2;
     {
-        const int waves = (P.num_tiles + kNumSMs - 1) / kNumSMs;
-        const double eff = (double)P.num_tiles / ((double)waves * kNumSMs);
-        const int tail = P.num_tiles - (P.num_tiles / kNumSMs) * kNumSMs;
-        P.sk = (!no_sk && g.causal == kCausalNone && P.num_tiles >= kNumSMs && eff < 0.9 && BN == 256 && tail > 0 &&
-                2 * tail <= kNumSMs && P.k_blocks >= 64) ? 1 : 0;  // measured: +4% at K=8192, -2% at K=2048
+        const int G = kNumSMs / CS;  // clusters
+        const int waves = (P.num_tiles + G - 1) / G;
+        const double eff = (double)P.num_tiles / ((double)waves * G);
+        const int tail = P.num_tiles - (P.num_tiles / G) * G;
+        P.sk = (!no_sk && (max_ctas <= 0 || max_ctas >= kNumSMs) && g.causal == kCausalNone && P.num_tiles >= G && eff < 0.9 && BN == 256 && tail > 0 &&
+                2 * tail <= G && P.k_blocks >= 64) ? 1 : 0;  // measured: +4% at K=8192, -2% at K=2048
     }
     if (P.sk) {
         static std::mutex mu;
@@ -1106,8 +1109,6 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         P.sk_epoch = ++epoch;
         if (P.sk_epoch == 0) P.sk_epoch = ++epoch;  // flags start at 0
     }
-    const int CS = (!no_cluster && !P.sk && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
-    if (CS > 1) P.num_tiles = ((P.tiles_m + CS - 1) / CS) * P.tiles_n * P.batch1 * P.batch2;
     CUtensorMap ma, mb;
     const bool ok_a = g.a_mn_major
                           ? make_map(&ma, g.A, g.M, g.K, g.lda, P.batch1, g.a_s1, P.batch2, g.a_s2, 64, 64)
