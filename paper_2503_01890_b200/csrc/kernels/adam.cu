@@ -12,8 +12,11 @@
 // Arithmetic is IEEE round-to-nearest with no contraction (explicit __f*_rn), in exactly
 // the order of oracle/adam_oracle.c and csrc/runtime/cpu_adam.cpp, so the GPU result is
 // bit-identical to both CPU implementations.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace ah {
 
@@ -139,6 +142,136 @@ adam_vec_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict_
     }
 }
 
+// TMA-fed variant (the default): a persistent CTA per SM streams tiles of kTile params
+// (p, m, v fp32 + g bf16 = 14 B/param) HBM -> shared memory with 1-D bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) issued by one producer thread into a kStages-deep
+// ring, so ~(kStages-1) x 28 KB of reads are in flight per SM independent of how many warps are
+// issuing arithmetic. 16 consumer warps read their 4 params per tile from shared memory
+// (conflict-free 16-B accesses), run the same IEEE arithmetic as adam_vec_kernel and write
+// p/m/v (+ bf16 p) straight to HBM with coalesced 16-B stores, then release the slot.
+constexpr int kTile = 2048;
+constexpr int kStages = 6;
+constexpr int kConsumerWarps = 16;
+constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
+constexpr size_t kStageBytes = (size_t)kTile * 14;
+constexpr size_t kTmaSmem = kStages * kStageBytes + 2 * kStages * 8;
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                         uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+        ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(policy)
+        : "memory");
+}
+
+template <bool kWriteBf16, bool kStats>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+adam_tma_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
+                const uint16_t* __restrict__ g, uint16_t* __restrict__ pout, size_t n_main,
+                AdamScalars k, const int* __restrict__ skip, float* __restrict__ stats) {
+    if (skip != nullptr && *skip != 0) return;
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+    uint64_t* empty = full + kStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t n_tiles = (n_main + kTile - 1) / kTile;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            tc::mbar_init(tc::smem_u32(&full[s]), 1);
+            tc::mbar_init(tc::smem_u32(&empty[s]), kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {  // producer
+        if (lane == 0) {
+            uint64_t policy;
+            asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(policy));
+            int s = 0;
+            uint32_t phase = 0;
+            for (size_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+                if (t >= blockIdx.x + (size_t)kStages * gridDim.x) tc::mbar_wait(tc::smem_u32(&empty[s]), phase ^ 1);
+                const size_t base = t * kTile;
+                const uint32_t cnt = (uint32_t)(n_main - base < (size_t)kTile ? n_main - base : kTile);
+                uint8_t* st = smem + s * kStageBytes;
+                const uint32_t bar = tc::smem_u32(&full[s]);
+                tc::mbar_expect_tx(bar, cnt * 14);
+                bulk_g2s(tc::smem_u32(st), p + base, cnt * 4, bar, policy);
+                bulk_g2s(tc::smem_u32(st + kTile * 4), m + base, cnt * 4, bar, policy);
+                bulk_g2s(tc::smem_u32(st + kTile * 8), v + base, cnt * 4, bar, policy);
+                bulk_g2s(tc::smem_u32(st + kTile * 12), g + base, cnt * 2, bar, policy);
+                if (++s == kStages) { s = 0; phase ^= 1; }
+            }
+        }
+        return;
+    }
+
+    Stat acc;
+    int s = 0;
+    uint32_t phase = 0;
+    const int e0 = threadIdx.x * 4;  // this thread's 4 params within the tile
+    for (size_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const size_t base = t * kTile;
+        const size_t cnt = n_main - base < (size_t)kTile ? n_main - base : kTile;
+        tc::mbar_wait(tc::smem_u32(&full[s]), phase);
+        const uint8_t* st = smem + s * kStageBytes;
+        if ((size_t)e0 < cnt) {  // cnt is a multiple of 8
+            float4 pp = *reinterpret_cast<const float4*>(st + e0 * 4);
+            float4 mm = *reinterpret_cast<const float4*>(st + kTile * 4 + e0 * 4);
+            float4 vv = *reinterpret_cast<const float4*>(st + kTile * 8 + e0 * 4);
+            const uint2 gw = *reinterpret_cast<const uint2*>(st + kTile * 12 + e0 * 2);
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[s]));
+            float* pv = &pp.x;
+            float* mv = &mm.x;
+            float* vq = &vv.x;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t w = e < 2 ? gw.x : gw.y;
+                const uint32_t bits = (e & 1) ? (w >> 16) : (w & 0xffffu);
+                const float gf = __fmul_rn(bf16_bits_to_f32(bits), k.inv_scale);
+                if (kStats) account(acc, gf);
+                adam_one(pv[e], mv[e], vq[e], gf, k);
+            }
+            st_f4(p + base + e0, pp);
+            st_f4(m + base + e0, mm);
+            st_f4(v + base + e0, vv);
+            if (kWriteBf16) {
+                const uint2 o = make_uint2(pack_bf16x2(pp.x, pp.y), pack_bf16x2(pp.z, pp.w));
+                asm volatile("st.global.L1::no_allocate.v2.u32 [%0], {%1,%2};" ::"l"(pout + base + e0), "r"(o.x),
+                             "r"(o.y)
+                             : "memory");
+            }
+        } else {
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(tc::smem_u32(&empty[s]));
+        }
+        if (++s == kStages) { s = 0; phase ^= 1; }
+    }
+    if (kStats) {
+        __shared__ float s_sum[kConsumerWarps];
+        __shared__ unsigned s_bad[kConsumerWarps];
+        const float ws = warp_sum(acc.sumsq);
+        const unsigned wb = warp_sum_u(acc.nonfinite);
+        if (lane == 0) {
+            s_sum[warp] = ws;
+            s_bad[warp] = wb;
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+        if (threadIdx.x < 32) {
+            float a = threadIdx.x < kConsumerWarps ? s_sum[threadIdx.x] : 0.f;
+            unsigned b = threadIdx.x < kConsumerWarps ? s_bad[threadIdx.x] : 0u;
+            a = warp_sum(a);
+            b = warp_sum_u(b);
+            if (threadIdx.x == 0) {
+                atomicAdd(stats, a);
+                if (b) atomicAdd(reinterpret_cast<unsigned*>(stats + 1), b);
+            }
+        }
+    }
+}
+
 // Scalar path: the < 8-element tail, or buffers that are not 16-byte aligned.
 __global__ void adam_scalar_kernel(float* p, float* m, float* v, const uint16_t* g,
                                    uint16_t* pout, size_t begin, size_t n, AdamScalars k,
@@ -233,7 +366,31 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
     size_t done = 0;
     if (vec) {
         const size_t n_vec = a.n / 8;
-        if (n_vec) {
+        static const bool use_tma = [] {
+            const char* e = std::getenv("AH_ADAM_KERNEL");
+            return !(e && e[0] == 'v');  // AH_ADAM_KERNEL=vec selects the register-streaming kernel
+        }();
+        if (n_vec && use_tma) {
+            const size_t tiles = (n_vec * 8 + kTile - 1) / kTile;
+            const int grid = (int)(tiles < (size_t)kNumSMs ? tiles : (size_t)kNumSMs);
+            static bool attr = [] {
+                cudaFuncSetAttribute(adam_tma_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                cudaFuncSetAttribute(adam_tma_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                cudaFuncSetAttribute(adam_tma_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                cudaFuncSetAttribute(adam_tma_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+                return true;
+            }();
+            (void)attr;
+            const size_t nm = n_vec * 8;
+            if (a.p_bf16 && a.stats)
+                adam_tma_kernel<true, true><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+            else if (a.p_bf16)
+                adam_tma_kernel<true, false><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+            else if (a.stats)
+                adam_tma_kernel<false, true><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+            else
+                adam_tma_kernel<false, false><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+        } else if (n_vec) {
             const int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
             if (a.p_bf16 && a.stats)
                 adam_vec_kernel<true, true><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
