@@ -152,6 +152,18 @@ int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_
                            uint16_t* dqkv, int32_t batch, int32_t seq_len, int32_t heads, int32_t head_dim,
                            void* stream);
 
+/* LayerNorm of the block step (part of OpKind::Forward / Backward / Recompute; no reference
+ * kernel — the reference times the whole block as t_fp / t_bp, workload.cpp:55-67).
+ * x, y [rows, h] bf16; gamma, beta [h] bf16; mean, rstd [rows] fp32 (eps 1e-5). */
+int ah_layernorm_fwd(const uint16_t* x, const uint16_t* gamma, const uint16_t* beta, uint16_t* y,
+                     float* mean, float* rstd, int32_t rows, int32_t h, void* stream);
+/* dx = LN'(dy) (+ dres if non-null); dgamma_dbeta [2h] = [sum dy*xhat | sum dy] (bf16).
+ * Optional fused bias gradients (h % 256 == 0): dres_colsum [h] = column sums of dres,
+ * dx_colsum [h] = column sums of bf16(dx). Deterministic (fixed-order reductions). */
+int ah_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd,
+                     const uint16_t* gamma, const uint16_t* dres, uint16_t* dx, uint16_t* dgamma_dbeta,
+                     uint16_t* dres_colsum, uint16_t* dx_colsum, int32_t rows, int32_t h, void* stream);
+
 /* ---------------------------------------------------------------------------------------
  * Training executor: one GPT iteration = hetsim::build_iteration_ops(profile, strategy, k)
  * (proj/core/src/simulator.cpp:91-229) executed on B200 in the per-lane order of

@@ -5,6 +5,8 @@
 // All HBM-bound: 16-byte vector access, one warp per row where rows are reduced, fp32 math,
 // bf16 storage. Every reduction has a fixed order (no float atomics) so recompute and
 // offload plans reproduce bit-identical training state.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "gpt_kernels.h"
 #include "kernels.h"
@@ -467,8 +469,18 @@ cudaError_t embed_fwd(const int* tok, const uint16_t* wte, const uint16_t* wpe, 
     return launched(1);
 }
 
+bool ln_rows_enabled(int h) {
+    static const bool on = [] {
+        const char* e = std::getenv("AH_LN");
+        return !(e && e[0] == 'w');  // AH_LN=warp selects the warp-per-row kernels
+    }();
+    return on && ln_rows_supported(h);
+}
+
 cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean, float* rstd,
                    int T, int h, cudaStream_t st) {
+    if (ln_rows_enabled(h) && ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y)) & 15u) == 0)
+        return ln_fwd_rows(x, g, b, y, mean, rstd, T, h, st);
     ln_fwd_kernel<<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T, h);
     return launched(1);
 }
@@ -819,6 +831,10 @@ int reduce_chunks(int T) { return T >= 4096 ? 64 : (T >= 512 ? 32 : 1); }
 
 cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
                     const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st) {
+    const uintptr_t al = reinterpret_cast<uintptr_t>(dy) | reinterpret_cast<uintptr_t>(x) |
+                         reinterpret_cast<uintptr_t>(dx) | reinterpret_cast<uintptr_t>(dres);
+    if (ln_rows_enabled(h) && (al & 15u) == 0)
+        return ln_bwd_rows(dy, x, mean, rstd, g, dres, dx, dgdb, nullptr, nullptr, part, T, h, st);
     ln_bwd_dx_kernel<<<(T + 7) / 8, 256, 0, st>>>(dy, x, mean, rstd, g, dres, dx, T, h);
     const int R = reduce_chunks(T), rows = (T + R - 1) / R;
     if (h % 8 == 0)

@@ -21,6 +21,18 @@ cudaError_t ln_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, con
 int reduce_chunks(int T);
 cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
                     const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st);
+// Row-parallel LayerNorm (ln_rows.cu): one CTA of h/8 threads per row chunk, rows read once.
+// ln_fwd / ln_bwd2 dispatch here when ln_rows_enabled(h) (h % 256 == 0; AH_LN=warp disables).
+bool ln_rows_supported(int h);
+bool ln_rows_enabled(int h);
+cudaError_t ln_fwd_rows(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean,
+                        float* rstd, int T, int h, cudaStream_t st);
+// Fused backward: dx (+ dres), dgdb = [dgamma | dbeta], and optionally the bias gradients
+// dres_colsum = sum over rows of dres (needs dres) and dx_colsum = sum over rows of bf16(dx).
+// part: >= ln_bwd_ctas(T) * 4h floats.
+cudaError_t ln_bwd_rows(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd,
+                        const uint16_t* g, const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, uint16_t* dres_colsum,
+                        uint16_t* dx_colsum, float* part, int T, int h, cudaStream_t st);
 // Column sums of X[T][N] (row stride ldx) -> out[N] (bf16 or fp32); part: >= colsum_rows(T)*N floats.
 int colsum_rows(int T);
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);

@@ -265,17 +265,22 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         AH_TRY(gemm::run(g, st));
     }
     AH_TRY(gemm::run(linear_wgrad(d, dy, h, a.gelu, 4 * h, W + o.w_fc2), st));  // dWfc2 -> slot
-    AH_TRY(gpt::colsum(dy, T, h, h, ws.part, W + o.b_fc2, 0, st));
+    const bool ln_fused = gpt::ln_rows_enabled(h);  // b_fc2 / b_proj grads come out of the LN2 backward
+    if (!ln_fused) AH_TRY(gpt::colsum(dy, T, h, h, ws.part, W + o.b_fc2, 0, st));
     // ---- MLP in: fc_pre = ln2 Wfc^T + b_fc
     AH_TRY(gemm::run(linear_dgrad(d, ws.d4h, 4 * h, W + o.w_fc, h, ws.dln), st));
     AH_TRY(gemm::run(linear_wgrad(d, ws.d4h, 4 * h, a.ln2, h, W + o.w_fc), st));
     AH_TRY(gpt::colsum(ws.d4h, T, 4 * h, 4 * h, ws.part, W + o.b_fc, 0, st));
     // ---- LN2 (+ residual path dy)
-    AH_TRY(gpt::ln_bwd2(ws.dln, a.x2, a.mean2, a.rstd2, W + o.ln2_g, dy, ws.dx2, W + o.ln2_g, ws.part, T, h, st));
+    if (ln_fused)  // dx2 = LN2'(dln) + dy; dgamma/dbeta; b_fc2 grad = colsum(dy); b_proj grad = colsum(dx2)
+        AH_TRY(gpt::ln_bwd_rows(ws.dln, a.x2, a.mean2, a.rstd2, W + o.ln2_g, dy, ws.dx2, W + o.ln2_g, W + o.b_fc2,
+                                W + o.b_proj, ws.part, T, h, st));
+    else
+        AH_TRY(gpt::ln_bwd2(ws.dln, a.x2, a.mean2, a.rstd2, W + o.ln2_g, dy, ws.dx2, W + o.ln2_g, ws.part, T, h, st));
     // ---- attention out-projection: x2 = x_in + att Wproj^T + b_proj
     AH_TRY(gemm::run(linear_dgrad(d, ws.dx2, h, W + o.w_proj, h, ws.datt), st));
     AH_TRY(gemm::run(linear_wgrad(d, ws.dx2, h, a.att, h, W + o.w_proj), st));
-    AH_TRY(gpt::colsum(ws.dx2, T, h, h, ws.part, W + o.b_proj, 0, st));
+    if (!ln_fused) AH_TRY(gpt::colsum(ws.dx2, T, h, h, ws.part, W + o.b_proj, 0, st));
     // ---- attention core, per (head, sequence)
     const bool fused = fused_attention(d);
     if (attention_mode(d) == AttnMode::Flash) {  // P recomputed from lse; dS (-> HBM for dQ), dV, dK
