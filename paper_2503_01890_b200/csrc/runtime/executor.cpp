@@ -105,6 +105,7 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     check(cudaStreamCreateWithPriority(&s_d2h_, cudaStreamNonBlocking, lo), "stream");
     plan(cfg);
     allocate_and_init();
+    check(cudaGetDevice(&device_), "get device");
     for (int l = 0; l < 4; ++l) lanes_[l] = std::thread([this, l] { lane_main(l); });
 }
 
@@ -382,6 +383,9 @@ void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate) {
 
 void Trainer::lane_main(int lane) {
     try {
+        // A new host thread starts on device 0: bind it to this trainer's device (one rank per
+        // GPU under DP), or its launches / stream-ordered allocations would target GPU 0.
+        check(cudaSetDevice(device_), "lane set device");
         long long next = 1;
         while (true) {
             Iter* it = nullptr;

@@ -69,6 +69,7 @@ private:
     friend struct CheckpointIO;
     // data parallel
     int dp_rank_ = 0, dp_size_ = 1;
+    int device_ = 0;  // the caller's current device at construction; every lane thread binds to it
     bool dp_ = false;      // collectives on
     void* comm_ = nullptr; // ncclComm_t
     size_t shard_ = 0;     // per-rank shard length of a block vector (elements, padded)
