@@ -24,6 +24,7 @@
 // 4-11 softmax / epilogue. Shapes: head_dim = 128, seq_len % 128 == 0.
 #include <cuda.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -267,6 +268,274 @@ flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
             for (int k8 = 0; k8 < 4; ++k8)
                 op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
                                     pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Persistent forward (the default): one CTA per SM walks a snake-ordered list of
+// (query tile, head, sequence) items, heavy (long causal) items first, and keeps the pipeline
+// full across items: Q is double-buffered per item, the K/V ring and the two TMEM score buffers
+// continue across item boundaries, and the next item's first score tile is issued while the
+// softmax warps run the current item's epilogue. P_j (bf16) is written back by the softmax warps
+// into the first 64 columns of its own score buffer and fed to O += P_j V_j straight from TMEM
+// (tcgen05.mma A-from-TMEM), so P never touches shared memory and softmax j+1 never waits for
+// the P V MMA of tile j (the score buffer of j is only reused by S_{j+2}, which the MMA thread
+// issues after P_j V_j: tcgen05.mma executes in issue order).
+__device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+struct FwdItems {
+    int nqt, nh, B, total, G, c;
+    __device__ int count() const {  // items of CTA c
+        const int full = total / G, rem = total % G;
+        int k = full;
+        if (rem) k += ((full & 1) == 0 ? c < rem : (G - 1 - c) < rem) ? 1 : 0;
+        return k;
+    }
+    __device__ void get(int k, int& qt, int& head, int& b) const {  // k-th item of CTA c (snake order)
+        const int w = k * G + ((k & 1) == 0 ? c : G - 1 - c);
+        const int per = nh * B;
+        qt = nqt - 1 - w / per;
+        const int rem = w % per;
+        head = rem % nh;
+        b = rem / nh;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const FwdParams A) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sQ = sm;              // [2] per item
+    uint8_t* sK = sm + 2 * kTile;  // [2]
+    uint8_t* sV = sm + 4 * kTile;  // [2]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kTile);
+    uint64_t* q_full = bar;        // [2]
+    uint64_t* q_empty = bar + 2;   // [2]
+    uint64_t* k_full = bar + 4;    // [2]
+    uint64_t* k_empty = bar + 6;   // [2]
+    uint64_t* v_full = bar + 8;    // [2]
+    uint64_t* v_empty = bar + 10;  // [2]
+    uint64_t* s_full = bar + 12;   // [2]
+    uint64_t* s_free = bar + 14;   // [2]
+    uint64_t* p_full = bar + 16;
+    uint64_t* pv_done = bar + 17;
+    uint64_t* o_full = bar + 18;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 20);
+    float* xmax = reinterpret_cast<float*>(bar + 22);  // [2 parity][2 halves][128 rows]
+    float* xsum = xmax + 2 * 2 * 128;                  // [2 halves][128 rows]
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    FwdItems items{A.s / kT, A.nh, A.B, (A.s / kT) * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
+    const int n_items = items.count();
+
+    if (warp == 0 && lane == 0) {
+        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&q_full[i]), 1);
+            mbar_init(smem_u32(&q_empty[i]), 1);
+            mbar_init(smem_u32(&k_full[i]), 1);
+            mbar_init(smem_u32(&k_empty[i]), 1);
+            mbar_init(smem_u32(&v_full[i]), 1);
+            mbar_init(smem_u32(&v_empty[i]), 1);
+            mbar_init(smem_u32(&s_full[i]), 1);
+            mbar_init(smem_u32(&s_free[i]), 8);
+        }
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(pv_done), 1);
+        mbar_init(smem_u32(o_full), 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_holder;  // S/P[0] 0-127, S/P[1] 128-255, O 256-383
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            uint32_t g = 0;
+            for (int it = 0; it < n_items; ++it) {
+                int qt, head, b;
+                items.get(it, qt, head, b);
+                const int qs = it & 1;
+                mbar_wait(smem_u32(&q_empty[qs]), ((it >> 1) & 1) ^ 1);
+                mbar_expect_tx(smem_u32(&q_full[qs]), kTile);
+                load_tile(smem_u32(sQ + qs * kTile), &tmQ, smem_u32(&q_full[qs]), qt * kT, head, b);
+                for (int j = 0; j <= qt; ++j, ++g) {
+                    const int st = g & 1;
+                    const uint32_t ph = (g >> 1) & 1;
+                    mbar_wait(smem_u32(&k_empty[st]), ph ^ 1);
+                    mbar_expect_tx(smem_u32(&k_full[st]), kTile);
+                    load_tile(smem_u32(sK + st * kTile), &tmK, smem_u32(&k_full[st]), j * kT, head, b);
+                    mbar_wait(smem_u32(&v_empty[st]), ph ^ 1);
+                    mbar_expect_tx(smem_u32(&v_full[st]), kTile);
+                    load_tile(smem_u32(sV + st * kTile), &tmV, smem_u32(&v_full[st]), j * kT, head, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer: S(g+1) ahead of P(g) V(g), across items =====
+            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+            constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (MN-major)
+            // cursor over this CTA's tiles: (item, j) and the global tile index g
+            int s_it = 0, s_j = 0, s_qt = 0;
+            uint32_t s_g = 0;
+            auto issue_next_S = [&]() {  // S of the tile at the S cursor, then advance it
+                const int qs = s_it & 1, st = s_g & 1;
+                const uint32_t ph = (s_g >> 1) & 1;
+                if (s_j == 0) {
+                    int h_, b_;
+                    items.get(s_it, s_qt, h_, b_);
+                    mbar_wait(smem_u32(&q_full[qs]), (s_it >> 1) & 1);
+                }
+                mbar_wait(smem_u32(&k_full[st]), ph);
+                mbar_wait(smem_u32(&s_free[st]), ph ^ 1);
+                fence_after();
+                const uint32_t qa = smem_u32(sQ + qs * kTile), ka = smem_u32(sK + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + st * 128, kdesc(qa, t), kdesc(ka, t), idS, t > 0);
+                commit(smem_u32(&s_full[st]));
+                commit(smem_u32(&k_empty[st]));
+                if (s_j == s_qt) {  // last score tile of the item: its Q buffer is free after this MMA
+                    commit(smem_u32(&q_empty[qs]));
+                    s_j = 0;
+                    ++s_it;
+                } else {
+                    ++s_j;
+                }
+                ++s_g;
+            };
+            if (n_items > 0) issue_next_S();
+            uint32_t g = 0;
+            for (int it = 0; it < n_items; ++it) {
+                int qt, head, b;
+                items.get(it, qt, head, b);
+                for (int j = 0; j <= qt; ++j, ++g) {
+                    if (s_it < n_items) issue_next_S();  // scores of the next tile overlap softmax of this one
+                    const int st = g & 1;
+                    mbar_wait(smem_u32(p_full), g & 1);
+                    mbar_wait(smem_u32(&v_full[st]), (g >> 1) & 1);
+                    fence_after();
+                    const uint32_t va = smem_u32(sV + st * kTile);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        mma_f16_ts(tmem + 256, tmem + st * 128 + t * 8, mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
+                    commit(smem_u32(pv_done));
+                    commit(smem_u32(&v_empty[st]));
+                }
+                commit(smem_u32(o_full));
+            }
+        }
+    } else if (warp >= 4) {  // ===== online softmax / epilogue =====
+        const int half = (warp - 4) >> 2, quarter = warp & 3;
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+        const int pair_bar = 1 + quarter;  // named barrier of warps (quarter, quarter + 4)
+        const float sl2 = A.sl2;
+        uint32_t g = 0;
+        for (int it = 0; it < n_items; ++it) {
+            int qt, head, b;
+            items.get(it, qt, head, b);
+            const int q = qt * kT + r;
+            float m_used = -INFINITY, l = 0.f;
+            for (int j = 0; j <= qt; ++j, ++g) {
+                const int st = g & 1;
+                mbar_wait(smem_u32(&s_full[st]), (g >> 1) & 1);
+                fence_after();
+                float v[64];
+                ld64(tmem + lane_base + st * 128 + half * 64, v);
+                if (j == qt) {  // diagonal tile: keys > q are masked
+                    const int lim = q - j * kT - half * 64;
+#pragma unroll
+                    for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
+                }
+                float cm = v[0];
+#pragma unroll
+                for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+                xmax[(st * 2 + half) * 128 + r] = cm;
+                fence_before();
+                // both halves have their scores in registers past this barrier: P may overwrite S
+                asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+                fence_after();
+                if (lane == 0) mbar_arrive(smem_u32(&s_free[st]));
+                const float mt = fmaxf(cm, xmax[(st * 2 + (half ^ 1)) * 128 + r]);  // finite: key 0 <= q
+                float alpha = 1.f;
+                bool rescale = false;
+                if (m_used == -INFINITY) {
+                    m_used = mt;
+                } else if ((mt - m_used) * sl2 > kRescaleLog2) {
+                    alpha = ex2_approx((m_used - mt) * sl2);
+                    l *= alpha;
+                    m_used = mt;
+                    rescale = true;
+                }
+                const float mb = m_used * sl2;
+                float w[32];  // packed bf16 pairs, bit-cast to float for tcgen05.st
+                float add = 0.f;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
+                    add += p0 + p1;
+                    w[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
+                }
+                l += add;
+                if (__any_sync(0xffffffffu, rescale)) {  // O += P V of tile g-1 must have landed
+                    mbar_wait(smem_u32(pv_done), (g - 1) & 1);
+                    fence_after();
+#pragma unroll 1
+                    for (int c = 0; c < 2; ++c) {
+                        float o[32];
+                        const uint32_t ta = tmem + lane_base + 256 + half * 64 + c * 32;
+                        ld32(ta, o);
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) o[i] *= alpha;
+                        st32(ta, o);
+                    }
+                }
+                st32(tmem + lane_base + st * 128 + half * 32, w);  // P_j -> first 64 columns of its S buffer
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(p_full));
+            }
+            xsum[half * 128 + r] = l;
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+            const float lt = l + xsum[(half ^ 1) * 128 + r];
+            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // xsum reused by the next item
+            const float inv = 1.f / lt;
+            if (half == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
+            mbar_wait(smem_u32(o_full), it & 1);
+            fence_after();
+            uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + half * 64;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+                float v[32];
+                ld32(tmem + lane_base + 256 + half * 64 + c * 32, v);
+                uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8)
+                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
+                                        pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+            }
+            fence_before();  // O reads complete before this warp's next P arrival lets P V overwrite O
         }
     }
     fence_before();
@@ -577,11 +846,24 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     a.sl2 = scale * 1.4426950408889634f;
     a.O = O;
     a.lse2 = lse2;
-    const size_t smem = 1024 + 6 * (size_t)kTile + 18 * 8 + 6 * 128 * 4;
-    static bool cfg = false;
-    cudaError_t e = set_smem(flash_fwd_kernel, smem, cfg);
+    static const bool v1 = [] {
+        const char* e = std::getenv("AH_FLASH_FWD");
+        return e && e[0] == 'v' && e[1] == '1';  // AH_FLASH_FWD=v1: one CTA per (tile, head, sequence)
+    }();
+    if (v1) {
+        const size_t smem = 1024 + 6 * (size_t)kTile + 18 * 8 + 6 * 128 * 4;
+        static bool cfg = false;
+        cudaError_t e = set_smem(flash_fwd_kernel, smem, cfg);
+        if (e != cudaSuccess) return e;
+        flash_fwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, a);
+        return launched(1);
+    }
+    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 6 * 128 * 4;
+    static bool cfg2 = false;
+    cudaError_t e = set_smem(flash_fwd_pk_kernel, smem, cfg2);
     if (e != cudaSuccess) return e;
-    flash_fwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, a);
+    const int items = (s / kT) * nh * B;
+    flash_fwd_pk_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, a);
     return launched(1);
 }
 

@@ -958,6 +958,17 @@ struct TimingState {
         double flops;
     };
     std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;  // pre-created timing events: no cudaEventCreate on the launch path
+    cudaEvent_t take() {
+        if (pool.empty()) {
+            cudaEvent_t e = nullptr;
+            cudaEventCreate(&e);
+            return e;
+        }
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
 };
 static TimingState& timing() {
     static TimingState t;
@@ -967,6 +978,11 @@ static TimingState& timing() {
 void timing_enable(bool on) {
     std::lock_guard<std::mutex> lk(timing().mu);
     timing().on = on;
+    while (on && timing().pool.size() < 16384) {  // enough for a timed bench region
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreate(&e) != cudaSuccess) break;
+        timing().pool.push_back(e);
+    }
 }
 
 void timing_collect(double* total_ms, double* total_flops, long long* launches) {
@@ -981,8 +997,8 @@ void timing_collect(double* total_ms, double* total_flops, long long* launches) 
             fl += r.flops;
             ++n;
         }
-        cudaEventDestroy(r.a);
-        cudaEventDestroy(r.b);
+        timing().pool.push_back(r.a);
+        timing().pool.push_back(r.b);
     }
     timing().recs.clear();
     if (total_ms) *total_ms = ms;
@@ -1136,12 +1152,12 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     {
         std::lock_guard<std::mutex> lk(timing().mu);
         timed = timing().on;
+        if (timed) {
+            ta = timing().take();
+            tb = timing().take();
+        }
     }
-    if (timed) {
-        cudaEventCreate(&ta);
-        cudaEventCreate(&tb);
-        cudaEventRecord(ta, stream);
-    }
+    if (timed) cudaEventRecord(ta, stream);
     cudaError_t e;
     if (BN == 256)
         e = CS == 2 ? launch_cfg<256, 6, 2>(ma, mb, mc, P, grid, stream) : launch_cfg<256, 4, 1>(ma, mb, mc, P, grid, stream);

@@ -16,6 +16,7 @@
 #include "hetsim/workload.hpp"
 
 #include <nccl.h>
+#include <cstdlib>
 
 namespace ah {
 
@@ -103,6 +104,13 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     check(cudaStreamCreateWithPriority(&s_compute_, cudaStreamNonBlocking, hi), "stream");
     check(cudaStreamCreateWithPriority(&s_h2d_, cudaStreamNonBlocking, lo), "stream");
     check(cudaStreamCreateWithPriority(&s_d2h_, cudaStreamNonBlocking, lo), "stream");
+    check(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
+    check(cudaEventCreateWithFlags(&ev_c2s_, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&ev_s2c_, cudaEventDisableTiming), "event");
+    {
+        const char* e = std::getenv("AH_PREFETCH_WEIGHTS");
+        prefetch_mat_ = !(e && e[0] == '0');
+    }
     plan(cfg);
     allocate_and_init();
     check(cudaGetDevice(&device_), "get device");
@@ -153,6 +161,11 @@ Trainer::~Trainer() {
     if (tok_host_) cudaFreeHost(tok_host_);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_h2d_);
+    cudaStreamDestroy(s_side_);
+    cudaEventDestroy(ev_c2s_);
+    cudaEventDestroy(ev_s2c_);
+    for (BlockState& b : blocks_)
+        if (b.mat_ev) cudaEventDestroy(b.mat_ev);
     cudaStreamDestroy(s_d2h_);
 }
 
@@ -359,10 +372,11 @@ Trainer::RtOp* Trainer::find(long long iter, const OpKey& key) {
     return nullptr;
 }
 
-void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate) {
+void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side) {
     if (iter < 1) return;
     cudaEvent_t ev = nullptr;
     int dep_lane = 0;
+    bool on_side = false;
     {
         std::unique_lock<std::mutex> lk(mu_);
         RtOp* d = find(iter, key);
@@ -373,8 +387,11 @@ void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate) {
         if (stop_) return;
         if (d->lane == kCpu) return;  // host ordering already established
         ev = gate ? d->start_ev : d->done_ev;
+        on_side = d->done_on_side;
     }
-    if (dep_lane == lane && !gate) return;  // same in-order stream
+    // same in-order stream, unless the consumer needs the dependency's side-stream tail
+    // (GpuOptim reads the reduce-scattered gradient of its backward)
+    if (dep_lane == lane && !gate && !(needs_side && on_side)) return;
     if (lane == kCpu)
         check(cudaEventSynchronize(ev), "event sync");
     else
@@ -397,9 +414,11 @@ void Trainer::lane_main(int lane) {
                     if (x->k == next) it = x;
             }
             if (!it) throw std::logic_error("executor: iteration window lost");
-            for (const OpKey& key : it->lane_order[lane]) {
+            for (size_t idx = 0; idx < it->lane_order[lane].size(); ++idx) {
+                const OpKey& key = it->lane_order[lane][idx];
                 RtOp& op = it->ops.at(key);
-                for (const auto& dp : op.deps) wait_dep(lane, dp.first, dp.second, false);
+                const bool needs_side = op.kind == OpKind::GpuOptim;
+                for (const auto& dp : op.deps) wait_dep(lane, dp.first, dp.second, false, needs_side);
                 for (const auto& gt : op.gates) wait_dep(lane, gt.first, gt.second, true);
                 if (lane == kCpu) {
                     {
@@ -425,14 +444,16 @@ void Trainer::lane_main(int lane) {
                     op.state = 1;
                 }
                 cv_.notify_all();
-                if (lane == kCompute)
+                if (lane == kCompute) {
+                    prefetch_weights(*it, idx);  // the next op's weights, overlapping this op
                     run_compute(*it, op);
+                }
                 else if (lane == kH2D)
                     run_h2d(*it, op);
                 else
                     run_d2h(*it, op);
                 check(cudaEventRecord(op.t1, st), "record");
-                check(cudaEventRecord(op.done_ev, st), "record");
+                check(cudaEventRecord(op.done_ev, op.done_on_side ? s_side_ : st), "record");
                 {
                     std::lock_guard<std::mutex> lk(mu_);
                     op.state = 2;
@@ -522,9 +543,11 @@ void Trainer::embed_backward_and_update(Iter& it) {
     check(gpt::embed_bwd_pos(dx0, dwpe_, d_.B, d_.s, h, st), "pos bwd");
     const size_t nwte = (size_t)d_.Vp * h, nwpe = (size_t)d_.s * h;
     if (dp_) {  // replicated embedding / positions / final LN: sum gradients over ranks
-        dp_allreduce_f32(dwte_, nwte, st);
-        dp_allreduce_f32(dwpe_, nwpe, st);
-        dp_allreduce_bf16(dlnf_b_, 2 * (size_t)h, st);
+        side_after_compute();
+        dp_allreduce_f32(dwte_, nwte, s_side_);
+        dp_allreduce_f32(dwpe_, nwpe, s_side_);
+        dp_allreduce_bf16(dlnf_b_, 2 * (size_t)h, s_side_);
+        compute_after_side();
     }
     check(gpt::f32_to_bf16(dwte_, dwte_b_, nwte, st), "cvt");
     check(gpt::f32_to_bf16(dwpe_, dwpe_b_, nwpe, st), "cvt");
@@ -547,15 +570,23 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
     const size_t off = shard_ * (size_t)dp_rank_;
     auto materialize = [&]() {  // bf16 weights from the on-GPU fp32 master (footnote 2)
         check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, st), "alloc wbuf");
-        if (dp_) {  // own shard, then all-gather the others over NVLink
+        if (dp_) {  // own shard, then all-gather the others over NVLink (side stream)
             check(launch_cast_f32_bf16(b.master, b.wbuf + off, shard_, st), "cast");
-            dp_gather(b.wbuf, st);
+            side_after_compute();
+            dp_gather(b.wbuf, s_side_);
+            compute_after_side();
         } else {
             check(launch_cast_f32_bf16(b.master, b.wbuf, mp, st), "cast");
         }
     };
+    if (b.mat_pending) {  // materialised ahead on the side stream (prefetch_weights)
+        check(cudaStreamWaitEvent(st, b.mat_ev, 0), "wait materialised weights");
+        b.mat_pending = false;
+    }
     if (b.needs_gather && op.kind != OpKind::GpuOptim) {  // prefetched shard -> full weights
-        dp_gather(b.wbuf, st);
+        side_after_compute();
+        dp_gather(b.wbuf, s_side_);
+        compute_after_side();
         b.needs_gather = false;
     }
     auto alloc_acts = [&]() { check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts"); };
@@ -570,7 +601,7 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
     switch (op.kind) {
         case OpKind::Forward: {
             if (i == 1) embed_forward(it);
-            if (!b.o) materialize();
+            if (!b.o && !b.wbuf) materialize();
             if (!b.wbuf) throw std::logic_error("forward without resident weights");
             alloc_acts();
             const BlockActs a = BlockActs::carve(d_, b.acts);
@@ -593,9 +624,13 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             check(block_backward(d_, b.wbuf, x_[(size_t)i - 1], a, gx_[i & 1], gx_[(i - 1) & 1], ws_, st),
                   "block bwd");
             free_acts();
-            if (dp_) {  // full local grads -> this rank's reduced shard (in place)
-                if (full_len() > mp) check(cudaMemsetAsync(b.wbuf + mp, 0, (full_len() - mp) * 2, st), "pad");
-                dp_reduce_grads(b.wbuf, st);
+            if (dp_) {  // full local grads -> this rank's reduced shard (in place), on the side
+                // stream: the next block's backward overlaps it; GpuOptim / GradOffload wait on
+                // this op's done_ev, which is recorded behind the reduce-scatter
+                side_after_compute();
+                if (full_len() > mp) check(cudaMemsetAsync(b.wbuf + mp, 0, (full_len() - mp) * 2, s_side_), "pad");
+                dp_reduce_grads(b.wbuf, s_side_);
+                op.done_on_side = true;
             }
             if (i == 1) embed_backward_and_update(it);
             break;
@@ -648,6 +683,44 @@ void Trainer::run_cpu(Iter& it, RtOp& op) {
     const size_t n = dp_ ? shard_ : d_.m_p();
     cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);
     op.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+void Trainer::side_after_compute() {
+    check(cudaEventRecord(ev_c2s_, s_compute_), "record");
+    check(cudaStreamWaitEvent(s_side_, ev_c2s_, 0), "side wait");
+}
+
+void Trainer::compute_after_side() {
+    check(cudaEventRecord(ev_s2c_, s_side_), "record");
+    check(cudaStreamWaitEvent(s_compute_, ev_s2c_, 0), "compute wait");
+}
+
+// If the compute op after lane_order[idx] will materialise a GPU-resident block's bf16 weights
+// (F, R or B of a non-O, non-P block whose buffer is not live), do it now on the side stream —
+// cast from the fp32 master (+ DP all-gather) — so it overlaps op idx instead of preceding the
+// next op on the compute stream. Only the compute lane thread touches these blocks' buffers.
+void Trainer::prefetch_weights(const Iter& it, size_t idx) {
+    if (!prefetch_mat_) return;
+    const std::vector<OpKey>& order = it.lane_order[kCompute];
+    if (idx + 1 >= order.size()) return;
+    const OpKey& x = order[idx];
+    const OpKey& y = order[idx + 1];
+    const bool uses_weights = y.kind == (int)OpKind::Forward || y.kind == (int)OpKind::Recompute ||
+                              y.kind == (int)OpKind::Backward;
+    if (!uses_weights || y.block == x.block || y.block < 1 || y.block > d_.L) return;
+    BlockState& b = blocks_[(size_t)y.block];
+    if (b.o || b.p || b.wbuf || b.mat_pending) return;
+    side_after_compute();  // the master is final: every compute op enqueued so far precedes the cast
+    check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, s_side_), "alloc wbuf");
+    if (dp_) {
+        check(launch_cast_f32_bf16(b.master, b.wbuf + shard_ * (size_t)dp_rank_, shard_, s_side_), "cast");
+        dp_gather(b.wbuf, s_side_);
+    } else {
+        check(launch_cast_f32_bf16(b.master, b.wbuf, d_.m_p(), s_side_), "cast");
+    }
+    if (!b.mat_ev) check(cudaEventCreateWithFlags(&b.mat_ev, cudaEventDisableTiming), "event");
+    check(cudaEventRecord(b.mat_ev, s_side_), "record");
+    b.mat_pending = true;
 }
 
 void Trainer::dp_gather(uint16_t* wbuf, cudaStream_t st) {

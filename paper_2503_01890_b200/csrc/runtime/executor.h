@@ -100,6 +100,7 @@ private:
         cudaEvent_t done_ev = nullptr, start_ev = nullptr, t0 = nullptr, t1 = nullptr;
         int state = 0;  // 0 pending, 1 started (start_ev recorded), 2 issued (done_ev recorded), 3 done (host)
         double host_ms = 0.0;
+        bool done_on_side = false;  // DP backward: done_ev follows the gradient reduce-scatter on s_side_
     };
     struct Iter {
         long long k = 0;
@@ -119,13 +120,20 @@ private:
         uint16_t* wbuf = nullptr;       // device bf16 weights / grads while resident
         void* acts = nullptr;           // device activation set while live
         bool needs_gather = false;      // DP: wbuf holds only this rank's shard so far
+        cudaEvent_t mat_ev = nullptr;   // side-stream materialisation (cast [+ all-gather]) done
+        bool mat_pending = false;       // wbuf was materialised ahead on s_side_; compute must wait mat_ev
     };
 
     void plan(const ah_trainer_config& cfg);
     void allocate_and_init();
     void build_iteration(Iter& it);
     void lane_main(int lane);
-    void wait_dep(int lane, long long iter, const OpKey& key, bool gate);
+    void wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side = false);
+    // Side stream: materialisation of the next compute op's weights (overlapping the current
+    // op) and every NCCL collective, issued by the compute lane thread in op order.
+    void prefetch_weights(const Iter& it, size_t idx);
+    void side_after_compute();
+    void compute_after_side();
     RtOp* find(long long iter, const OpKey& key);
     void run_compute(Iter& it, RtOp& op);
     void run_h2d(Iter& it, RtOp& op);
@@ -151,6 +159,9 @@ private:
     std::vector<OpKey> order_[2][4];
 
     cudaStream_t s_compute_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
+    cudaStream_t s_side_ = nullptr;
+    cudaEvent_t ev_c2s_ = nullptr, ev_s2c_ = nullptr;  // reused: a wait binds to the latest record
+    bool prefetch_mat_ = true;
     std::vector<BlockState> blocks_;  // index 1..L
     std::vector<uint16_t*> x_;        // residual stream x[0..L] (x[0] = embedding output)
     uint16_t* gx_[2] = {nullptr, nullptr};  // residual-gradient ping-pong
