@@ -777,6 +777,290 @@ flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant_
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Persistent backward (the default): one CTA per SM walks a snake-ordered list of
+// (key tile, head, sequence) items, heavy (many query tiles) first. The Q / dO ring, the row
+// statistics and the S / dP / P-dS pipeline continue across item boundaries; the next item's
+// K / V load as soon as the current item's last S / dP MMAs have read K / V, and its first S / dP
+// MMAs are issued while the epilogue warps drain the current item's dV / dK accumulators.
+struct BwdItems {
+    int nt, nh, B, total, G, c;
+    __device__ int count() const {
+        const int full = total / G, rem = total % G;
+        int k = full;
+        if (rem) k += ((full & 1) == 0 ? c < rem : (G - 1 - c) < rem) ? 1 : 0;
+        return k;
+    }
+    __device__ void get(int k, int& kt, int& head, int& b) const {
+        const int w = k * G + ((k & 1) == 0 ? c : G - 1 - c);
+        const int per = nh * B;
+        kt = w / per;  // 0 = the most query tiles
+        const int rem = w % per;
+        head = rem % nh;
+        b = rem / nh;
+    }
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+flash_bwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                    const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sK = sm;
+    uint8_t* sV = sm + kTile;
+    uint8_t* sQ = sm + 2 * kTile;   // [2]
+    uint8_t* sdO = sm + 4 * kTile;  // [2]
+    uint8_t* sPS = sm + 6 * kTile;  // P_i, then dS_i
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kTile);
+    uint64_t* kv_full = bar;
+    uint64_t* st_full = bar + 1;   // [2]
+    uint64_t* st_empty = bar + 3;  // [2]
+    uint64_t* s_full = bar + 5;
+    uint64_t* s_free = bar + 6;
+    uint64_t* dp_full = bar + 7;
+    uint64_t* dp_free = bar + 8;
+    uint64_t* p_full = bar + 9;
+    uint64_t* pv_done = bar + 10;
+    uint64_t* ds_full = bar + 11;
+    uint64_t* ps_free = bar + 12;
+    uint64_t* acc_full = bar + 13;
+    uint64_t* kv_empty = bar + 14;
+    uint64_t* acc_free = bar + 15;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 16);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = A.s / kT;
+    BwdItems items{nt, A.nh, A.B, nt * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
+    const int n_items = items.count();
+
+    if (warp == 0 && lane == 0) {
+        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmdO})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+        mbar_init(smem_u32(kv_full), 1);
+        mbar_init(smem_u32(kv_empty), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&st_full[i]), 1);
+            mbar_init(smem_u32(&st_empty[i]), 1);
+        }
+        mbar_init(smem_u32(s_full), 1);
+        mbar_init(smem_u32(s_free), 8);
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(dp_free), 8);
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(pv_done), 1);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(ps_free), 1);
+        mbar_init(smem_u32(acc_full), 1);
+        mbar_init(smem_u32(acc_free), 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_holder;  // S 0-127, dP 128-255, dV 256-383, dK 384-511
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer =====
+            uint32_t g = 0;
+            for (int it = 0; it < n_items; ++it) {
+                int kt, head, b;
+                items.get(it, kt, head, b);
+                if (it > 0) mbar_wait(smem_u32(kv_empty), (it - 1) & 1);  // last S / dP of it-1 read K, V
+                mbar_expect_tx(smem_u32(kv_full), 2 * kTile);
+                load_tile(smem_u32(sK), &tmK, smem_u32(kv_full), kt * kT, head, b);
+                load_tile(smem_u32(sV), &tmV, smem_u32(kv_full), kt * kT, head, b);
+                for (int qi = kt; qi < nt; ++qi, ++g) {
+                    const int st = g & 1;
+                    mbar_wait(smem_u32(&st_empty[st]), ((g >> 1) & 1) ^ 1);
+                    const uint32_t fb = smem_u32(&st_full[st]);
+                    mbar_expect_tx(fb, 2 * kTile);
+                    load_tile(smem_u32(sQ + st * kTile), &tmQ, fb, qi * kT, head, b);
+                    load_tile(smem_u32(sdO + st * kTile), &tmdO, fb, qi * kT, head, b);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer =====
+            constexpr uint32_t idSS = idesc_bf16(128, 128, 0, 0);   // X (K-major) x Y^T (K-major)
+            constexpr uint32_t idACC = idesc_bf16(128, 128, 1, 1);  // X^T (MN-major) x Y (MN-major)
+            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), psa = smem_u32(sPS);
+            // S_g = Q_g K^T, dP_g = dO_g V^T; `first` = first tile of item `it` (waits its K / V);
+            // `last` = last tile of its item (K / V free once these MMAs complete)
+            auto issue_S_dP = [&](uint32_t g, int it, bool first, bool last) {
+                const int st = g & 1;
+                if (first) mbar_wait(smem_u32(kv_full), it & 1);
+                mbar_wait(smem_u32(&st_full[st]), (g >> 1) & 1);
+                mbar_wait(smem_u32(s_free), (g & 1) ^ 1);
+                fence_after();
+                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem, kdesc(qa, t), kdesc(ka, t), idSS, t > 0);
+                commit(smem_u32(s_full));
+                mbar_wait(smem_u32(dp_free), (g & 1) ^ 1);
+                fence_after();
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 128, kdesc(da, t), kdesc(va, t), idSS, t > 0);
+                commit(smem_u32(dp_full));
+                if (last) commit(smem_u32(kv_empty));
+            };
+            uint32_t g = 0;
+            if (n_items > 0) {
+                int kt0, h0, b0;
+                items.get(0, kt0, h0, b0);
+                issue_S_dP(0, 0, true, kt0 == nt - 1);
+            }
+            for (int it = 0; it < n_items; ++it) {
+                int kt, head, b;
+                items.get(it, kt, head, b);
+                const int nq = nt - kt;
+                if (it > 0) mbar_wait(smem_u32(acc_free), (it - 1) & 1);  // epilogue of it-1 read dV / dK
+                for (int i = 0; i < nq; ++i, ++g) {
+                    const int st = g & 1;
+                    const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
+                    mbar_wait(smem_u32(p_full), g & 1);
+                    fence_after();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        mma_f16(tmem + 256, mndesc(psa, t), mndesc(da, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
+                    commit(smem_u32(pv_done));
+                    if (i + 1 < nq) issue_S_dP(g + 1, it, false, i + 2 == nq);  // overlaps this tile's dS
+                    mbar_wait(smem_u32(ds_full), g & 1);
+                    fence_after();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        mma_f16(tmem + 384, mndesc(psa, t), mndesc(qa, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
+                    commit(smem_u32(&st_empty[st]));
+                    commit(smem_u32(ps_free));
+                }
+                commit(smem_u32(acc_full));
+                if (it + 1 < n_items) {  // next item's first scores overlap this item's epilogue
+                    int kn, hn, bn;
+                    items.get(it + 1, kn, hn, bn);
+                    issue_S_dP(g, it + 1, true, kn == nt - 1);
+                }
+            }
+        }
+    } else if (warp >= 4) {  // ===== P, dS; epilogue =====
+        const int half = (warp - 4) >> 2, quarter = warp & 3;  // keys [64 * half, 64 * half + 64)
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+        const float sl2 = A.sl2;
+        uint8_t* slab = sPS + half * (kTile / 2) + quarter * 4096;  // this warp's 32 rows x 64 keys
+        uint32_t g = 0;
+        for (int it = 0; it < n_items; ++it) {
+            int kt, head, b;
+            items.get(it, kt, head, b);
+            const int nq = nt - kt;
+            const size_t row0 = ((size_t)b * A.nh + head) * A.s + (size_t)kt * kT + r;
+            float lse_n = A.lse2[row0], D_n = A.D[row0];  // row statistics, prefetched one tile ahead
+            for (int i = 0; i < nq; ++i, ++g) {
+                const int qi = kt + i;
+                const int q = qi * kT + r;
+                const size_t row = row0 + (size_t)i * kT;
+                const float lse = lse_n, Dq = D_n;
+                if (i + 1 < nq) {
+                    lse_n = A.lse2[row + kT];
+                    D_n = A.D[row + kT];
+                }
+                mbar_wait(smem_u32(s_full), g & 1);
+                fence_after();
+                uint32_t w[32];
+                {
+                    float v[64];
+                    ld64(tmem + lane_base + half * 64, v);
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(s_free));
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        w[k] = pack_bf16x2_rn(ex2_approx(fmaf(v[2 * k], sl2, -lse)), ex2_approx(fmaf(v[2 * k + 1], sl2, -lse)));
+                }
+                if (qi == kt) {  // diagonal tile: keys > q have P = 0
+                    const int lim = q - kt * kT - half * 64;
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        w[k] &= (2 * k <= lim ? 0x0000ffffu : 0u) | (2 * k + 1 <= lim ? 0xffff0000u : 0u);
+                }
+                if (g > 0) {
+                    mbar_wait(smem_u32(ps_free), (g - 1) & 1);  // dK MMA of g-1 has read dS
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // and the dS store
+                    __syncwarp();
+                }
+                sts_row_half(sPS, half, r, w);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(p_full));
+                mbar_wait(smem_u32(dp_full), g & 1);
+                fence_after();
+                uint32_t o[32];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float v[32];
+                    ld32(tmem + lane_base + 128 + half * 64 + c * 32, v);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const uint32_t pw = w[c * 16 + k];
+                        const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
+                        o[c * 16 + k] = pack_bf16x2_rn(p0 * (v[2 * k] - Dq), p1 * (v[2 * k + 1] - Dq));
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(dp_free));
+                mbar_wait(smem_u32(pv_done), g & 1);  // dV MMA has read P
+                sts_row_half(sPS, half, r, o);
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(ds_full));
+                    asm volatile(
+                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                            reinterpret_cast<uint64_t>(&tmdS)),
+                        "r"(smem_u32(slab)), "r"(kt * kT + half * 64), "r"(qi * kT + quarter * 32), "r"(head), "r"(b)
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
+            }
+            mbar_wait(smem_u32(acc_full), it & 1);
+            fence_after();
+            // thread r = key row of the tile: dV, dK (x scale) -> dqkv
+            uint16_t* base = A.dqkv + ((size_t)b * A.s + (size_t)kt * kT + r) * 3 * A.h + (size_t)head * kHD + half * 64;
+#pragma unroll 1
+            for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
+                uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
+                const float f = which == 0 ? 1.f : A.scale;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    float v[32];
+                    ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
+                    uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int k8 = 0; k8 < 4; ++k8)
+                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
+                                            pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(acc_free));
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -889,11 +1173,24 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     a.D = D;
     a.dS = dS;
     a.dqkv = dqkv;
-    const size_t smem = 1024 + 7 * (size_t)kTile + 16 * 8;
-    static bool cfg = false;
-    e = set_smem(flash_bwd_kernel, smem, cfg);
+    static const bool v1 = [] {
+        const char* e = std::getenv("AH_FLASH_BWD");
+        return e && e[0] == 'v' && e[1] == '1';  // AH_FLASH_BWD=v1: one CTA per (key tile, head, sequence)
+    }();
+    if (v1) {
+        const size_t smem = 1024 + 7 * (size_t)kTile + 16 * 8;
+        static bool cfg = false;
+        e = set_smem(flash_bwd_kernel, smem, cfg);
+        if (e != cudaSuccess) return e;
+        flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
+        return launched(1);
+    }
+    const size_t smem = 1024 + 7 * (size_t)kTile + 18 * 8;
+    static bool cfg2 = false;
+    e = set_smem(flash_bwd_pk_kernel, smem, cfg2);
     if (e != cudaSuccess) return e;
-    flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
+    const int items = (s / kT) * nh * B;
+    flash_bwd_pk_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
     return launched(1);
 }
 
