@@ -46,6 +46,7 @@ extern "C" int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, co
         g.batch2 = batch;
         g.M = s; g.N = head_dim; g.K = s;
         g.A = dS; g.lda = s; g.a_s1 = s * s; g.a_s2 = (long long)heads * s * s;
+        g.a_mn_major = ah::gpt::flash_bwd_ds_transposed() ? 1 : 0;  // dS^T [key][query]
         g.B = qkv + h; g.b_mn_major = 1; g.ldb = 3 * h; g.b_s1 = head_dim; g.b_s2 = s * 3 * h;
         g.C = dqkv; g.ldc = 3 * h; g.c_s1 = head_dim; g.c_s2 = s * 3 * h;
         g.alpha = scale;

@@ -1061,6 +1061,293 @@ flash_bwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Transposed persistent backward (the default). Per (key tile, head, sequence) item and query
+// tile i, the scores are formed key-major, S^T = K Q_i^T and dP^T = V dO_i^T, so a softmax
+// thread owns one KEY row and the per-query statistics (lse2, D) are 128-float vectors that the
+// producer streams into shared memory next to Q_i / dO_i. P^T and dS^T are then exactly the
+// K-major A operands of dV += P^T dO_i and dK += dS^T Q_i: each half-warp writes its 64 query
+// columns (bf16 pairs) into the first 32 TMEM columns of its own half of the S^T / dP^T buffer
+// and the MMAs read A straight from TMEM — no shared-memory staging of P / dS, no cross-half
+// barrier (tcgen05.mma executes in issue order, so S^T_{i+1} / dP^T_{i+1} are issued after the
+// dV_i / dK_i that read the same columns). dS^T also goes to HBM for the deterministic
+// dQ = (dS^T)^T K GEMM (MN-major A). TMEM: S^T 0-127, dP^T 128-255, dV 256-383, dK 384-511.
+// (A variant staging P^T through a K-major smem tile so S^T_{i+1} could run before dV_i measured
+// 151 us vs 129 us for this one at B=8, s=1024, 16 heads.)
+// TMEM A operand of K step t (16 queries) inside a score buffer at column `base`: half h's
+// 64 queries sit in columns [base + 64h, base + 64h + 32).
+__device__ __forceinline__ void bulk_g2s_1d(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst), "l"(src), "r"(bytes), "r"(bar)
+                 : "memory");
+}
+__device__ __forceinline__ uint32_t tsA(uint32_t base, int t) { return base + (t >> 2) * 64 + (t & 3) * 8; }
+
+__global__ void __launch_bounds__(kThreads, 1)
+flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                   const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
+                   const BwdParams A) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* sm = align1024(smem_raw);
+    uint8_t* sK = sm;
+    uint8_t* sV = sm + kTile;
+    uint8_t* sQ = sm + 2 * kTile;   // [2]
+    uint8_t* sdO = sm + 4 * kTile;  // [2]
+    float* sStat = reinterpret_cast<float*>(sm + 6 * kTile);  // [2 stages][lse2 128 | D 128]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kTile + 2048);
+    uint64_t* kv_full = bar;
+    uint64_t* kv_empty = bar + 1;
+    uint64_t* st_full = bar + 2;   // [2]
+    uint64_t* st_empty = bar + 4;  // [2]
+    uint64_t* s_full = bar + 6;
+    uint64_t* s_free = bar + 7;
+    uint64_t* dp_full = bar + 8;
+    uint64_t* dp_free = bar + 9;
+    uint64_t* p_full = bar + 10;
+    uint64_t* ds_full = bar + 11;
+    uint64_t* acc_full = bar + 12;
+    uint64_t* acc_free = bar + 13;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 14);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = A.s / kT;
+    BwdItems items{nt, A.nh, A.B, nt * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
+    const int n_items = items.count();
+
+    if (warp == 0 && lane == 0) {
+        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmdO})
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+        mbar_init(smem_u32(kv_full), 1);
+        mbar_init(smem_u32(kv_empty), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&st_full[i]), 1);
+            mbar_init(smem_u32(&st_empty[i]), 1);
+        }
+        mbar_init(smem_u32(s_full), 1);
+        mbar_init(smem_u32(s_free), 8);
+        mbar_init(smem_u32(dp_full), 1);
+        mbar_init(smem_u32(dp_free), 8);
+        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(ds_full), 8);
+        mbar_init(smem_u32(acc_full), 1);
+        mbar_init(smem_u32(acc_free), 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_holder;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ===== TMA producer: K, V per item; Q, dO per query tile =====
+            uint32_t g = 0;
+            for (int it = 0; it < n_items; ++it) {
+                int kt, head, b;
+                items.get(it, kt, head, b);
+                if (it > 0) mbar_wait(smem_u32(kv_empty), (it - 1) & 1);
+                mbar_expect_tx(smem_u32(kv_full), 2 * kTile);
+                load_tile(smem_u32(sK), &tmK, smem_u32(kv_full), kt * kT, head, b);
+                load_tile(smem_u32(sV), &tmV, smem_u32(kv_full), kt * kT, head, b);
+                const size_t srow = ((size_t)b * A.nh + head) * A.s;
+                for (int qi = kt; qi < nt; ++qi, ++g) {
+                    const int st = g & 1;
+                    mbar_wait(smem_u32(&st_empty[st]), ((g >> 1) & 1) ^ 1);
+                    const uint32_t fb = smem_u32(&st_full[st]);
+                    mbar_expect_tx(fb, 2 * kTile + 1024);
+                    load_tile(smem_u32(sQ + st * kTile), &tmQ, fb, qi * kT, head, b);
+                    load_tile(smem_u32(sdO + st * kTile), &tmdO, fb, qi * kT, head, b);
+                    bulk_g2s_1d(smem_u32(sStat + st * 256), A.lse2 + srow + (size_t)qi * kT, 512, fb);
+                    bulk_g2s_1d(smem_u32(sStat + st * 256 + 128), A.D + srow + (size_t)qi * kT, 512, fb);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ===== MMA issuer: S^T(g+1), dV(g), dK(g), dP^T(g+1) =====
+            constexpr uint32_t idSS = idesc_bf16(128, 128, 0, 0);  // K (K-major) x Q^T (K-major)
+            constexpr uint32_t idAB = idesc_bf16(128, 128, 0, 1);  // P^T / dS^T (K-major) x dO / Q (MN-major)
+            const uint32_t ka = smem_u32(sK), va = smem_u32(sV);
+            // tile sequence of this CTA: g -> (item, first / last tile of the item)
+            int c_it = 0, c_i = 0, c_nq = 0;  // cursor of the next S^T to issue
+            uint32_t c_g = 0;
+            auto cursor_item = [&]() {
+                int kt, h_, b_;
+                items.get(c_it, kt, h_, b_);
+                c_nq = nt - kt;
+            };
+            auto issue_S = [&]() {  // S^T at the cursor = K Q^T, then advance the cursor
+                const uint32_t g = c_g;
+                const int st = g & 1;
+                if (c_i == 0) mbar_wait(smem_u32(kv_full), c_it & 1);
+                mbar_wait(smem_u32(&st_full[st]), (g >> 1) & 1);
+                mbar_wait(smem_u32(s_free), (g & 1) ^ 1);
+                fence_after();
+                const uint32_t qa = smem_u32(sQ + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem, kdesc(ka, t), kdesc(qa, t), idSS, t > 0);
+                commit(smem_u32(s_full));
+                ++c_g;
+                if (++c_i == c_nq) {
+                    c_i = 0;
+                    if (++c_it < n_items) cursor_item();
+                }
+            };
+            auto issue_dP = [&](uint32_t g, bool last) {  // dP^T_g = V dO_g^T (last: K / V free after it)
+                const int st = g & 1;
+                mbar_wait(smem_u32(dp_free), (g & 1) ^ 1);
+                fence_after();
+                const uint32_t da = smem_u32(sdO + st * kTile);
+#pragma unroll
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + 128, kdesc(va, t), kdesc(da, t), idSS, t > 0);
+                commit(smem_u32(dp_full));
+                if (last) commit(smem_u32(kv_empty));
+            };
+            if (n_items > 0) {
+                cursor_item();
+                const bool single = c_nq == 1;
+                issue_S();
+                issue_dP(0, single);
+            }
+            uint32_t g = 0;
+            for (int it = 0; it < n_items; ++it) {
+                int kt, head, b;
+                items.get(it, kt, head, b);
+                const int nq = nt - kt;
+                for (int i = 0; i < nq; ++i, ++g) {
+                    const int st = g & 1;
+                    const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
+                    if (i == 0 && it > 0) mbar_wait(smem_u32(acc_free), (it - 1) & 1);  // epilogue read dV / dK
+                    mbar_wait(smem_u32(p_full), g & 1);
+                    fence_after();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        mma_f16_ts(tmem + 256, tsA(tmem, t), mndesc(da, t), idAB, (i > 0 || t > 0) ? 1u : 0u);
+                    if (i + 1 < nq) issue_S();  // P^T_g consumed in order before S^T_{g+1}
+                    mbar_wait(smem_u32(ds_full), g & 1);
+                    fence_after();
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        mma_f16_ts(tmem + 384, tsA(tmem + 128, t), mndesc(qa, t), idAB, (i > 0 || t > 0) ? 1u : 0u);
+                    commit(smem_u32(&st_empty[st]));
+                    if (i + 1 < nq) {
+                        issue_dP(g + 1, i + 2 == nq);  // dS^T_g consumed in order before dP^T_{g+1}
+                    } else {
+                        commit(smem_u32(acc_full));
+                        if (it + 1 < n_items) {  // first dP^T of the next item overlaps this epilogue
+                            int kn, hn, bn;
+                            items.get(it + 1, kn, hn, bn);
+                            issue_S();
+                            issue_dP(g + 1, kn == nt - 1);
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4) {  // ===== P^T, dS^T (thread = key row); epilogue =====
+        const int half = (warp - 4) >> 2, quarter = warp & 3;  // queries [64 * half, 64 * half + 64)
+        const int r = quarter * 32 + lane;
+        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
+        const float sl2 = A.sl2;
+        uint32_t g = 0;
+        for (int it = 0; it < n_items; ++it) {
+            int kt, head, b;
+            items.get(it, kt, head, b);
+            const int nq = nt - kt;
+            uint16_t* dsrow = A.dS + (((size_t)b * A.nh + head) * A.s + (size_t)kt * kT + r) * A.s + half * 64;
+            for (int i = 0; i < nq; ++i, ++g) {
+                const int qi = kt + i;
+                const float* lse = sStat + (g & 1) * 256 + half * 64;  // 64 queries of this half
+                const float* Dv = lse + 128;
+                mbar_wait(smem_u32(s_full), g & 1);
+                fence_after();
+                uint32_t w[32];
+                {
+                    float v[64];
+                    ld64(tmem + lane_base + half * 64, v);
+                    fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(smem_u32(s_free));
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        const float4 l4 = reinterpret_cast<const float4*>(lse)[k];
+                        w[2 * k] = pack_bf16x2_rn(ex2_approx(fmaf(v[4 * k], sl2, -l4.x)), ex2_approx(fmaf(v[4 * k + 1], sl2, -l4.y)));
+                        w[2 * k + 1] = pack_bf16x2_rn(ex2_approx(fmaf(v[4 * k + 2], sl2, -l4.z)), ex2_approx(fmaf(v[4 * k + 3], sl2, -l4.w)));
+                    }
+                }
+                if (qi == kt) {  // diagonal tile: P = 0 where the query precedes the key
+                    const int lim = r - half * 64;  // keep query columns c >= lim
+#pragma unroll
+                    for (int k = 0; k < 32; ++k)
+                        w[k] &= (2 * k >= lim ? 0x0000ffffu : 0u) | (2 * k + 1 >= lim ? 0xffff0000u : 0u);
+                }
+                st32(tmem + lane_base + half * 64, *reinterpret_cast<float(*)[32]>(w));  // P^T -> TMEM
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(p_full));
+                mbar_wait(smem_u32(dp_full), g & 1);
+                fence_after();
+                uint32_t o[32];
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    float v[32];
+                    ld32(tmem + lane_base + 128 + half * 64 + c * 32, v);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float4 d4 = reinterpret_cast<const float4*>(Dv + c * 32)[k];
+                        const uint32_t p0 = w[c * 16 + 2 * k], p1 = w[c * 16 + 2 * k + 1];
+                        o[c * 16 + 2 * k] = pack_bf16x2_rn(__uint_as_float(p0 << 16) * (v[4 * k] - d4.x),
+                                                           __uint_as_float(p0 & 0xffff0000u) * (v[4 * k + 1] - d4.y));
+                        o[c * 16 + 2 * k + 1] = pack_bf16x2_rn(__uint_as_float(p1 << 16) * (v[4 * k + 2] - d4.z),
+                                                               __uint_as_float(p1 & 0xffff0000u) * (v[4 * k + 3] - d4.w));
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(dp_free));
+                st32(tmem + lane_base + 128 + half * 64, *reinterpret_cast<float(*)[32]>(o));  // dS^T -> TMEM
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(smem_u32(ds_full));
+                uint4* dst = reinterpret_cast<uint4*>(dsrow + (size_t)qi * kT);  // dS^T row -> HBM (dQ GEMM)
+#pragma unroll
+                for (int k8 = 0; k8 < 8; ++k8) dst[k8] = make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+            }
+            mbar_wait(smem_u32(acc_full), it & 1);
+            fence_after();
+            uint16_t* base = A.dqkv + ((size_t)b * A.s + (size_t)kt * kT + r) * 3 * A.h + (size_t)head * kHD + half * 64;
+#pragma unroll 1
+            for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
+                uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
+                const float f = which == 0 ? 1.f : A.scale;
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {
+                    float v[32];
+                    ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
+                    uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
+#pragma unroll
+                    for (int k8 = 0; k8 < 4; ++k8)
+                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
+                                            pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
+                }
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(acc_free));
+        }
+    }
+    fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1113,6 +1400,19 @@ cudaError_t set_smem(K kernel, size_t bytes, bool& done) {
 }  // namespace
 
 bool flash_supported(int hd, int s) { return hd == kHD && s % kT == 0 && s >= kT; }
+
+// AH_FLASH_BWD=v1: one CTA per (key tile, head, sequence); =pk: persistent, query-major scores
+// (dS [q][k]); default: persistent transposed (dS^T [k][q]).
+int flash_bwd_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("AH_FLASH_BWD");
+        if (e && e[0] == 'v' && e[1] == '1') return 0;
+        if (e && e[0] == 'p' && e[1] == 'k') return 1;
+        return 2;
+    }();
+    return v;
+}
+bool flash_bwd_ds_transposed() { return flash_bwd_variant() == 2; }
 
 cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
                       cudaStream_t st) {
@@ -1173,11 +1473,17 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     a.D = D;
     a.dS = dS;
     a.dqkv = dqkv;
-    static const bool v1 = [] {
-        const char* e = std::getenv("AH_FLASH_BWD");
-        return e && e[0] == 'v' && e[1] == '1';  // AH_FLASH_BWD=v1: one CTA per (key tile, head, sequence)
-    }();
-    if (v1) {
+    const int variant = flash_bwd_variant();
+    if (variant == 2) {  // transposed persistent kernel: dS^T [B][nh][key][query]
+        const size_t smem = 1024 + 6 * (size_t)kTile + 2048 + 16 * 8;
+        static bool cfg3 = false;
+        e = set_smem(flash_bwd_t_kernel, smem, cfg3);
+        if (e != cudaSuccess) return e;
+        const int items = (s / kT) * nh * B;
+        flash_bwd_t_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, mdo, a);
+        return launched(1);
+    }
+    if (variant == 0) {
         const size_t smem = 1024 + 7 * (size_t)kTile + 16 * 8;
         static bool cfg = false;
         e = set_smem(flash_bwd_kernel, smem, cfg);

@@ -57,6 +57,10 @@ cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, 
 bool flash_supported(int hd, int s);
 cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
                       cudaStream_t st);
+// The default flash backward writes dS TRANSPOSED, dS^T [B, nh, s(key), s(query)]: the dQ GEMM
+// then reads it as an MN-major A operand. flash_bwd_ds_transposed() says which layout is used.
+int flash_bwd_variant();
+bool flash_bwd_ds_transposed();
 cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2, float* D,
                       uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
 // Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.

@@ -315,6 +315,8 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         heads(g, d);
         g.M = s; g.N = hd; g.K = s;
         g.A = ws.dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)d.nh * s * s;
+        // the default flash backward stores dS^T [key][query]: read it as an MN-major A
+        g.a_mn_major = attention_mode(d) == AttnMode::Flash && gpt::flash_bwd_ds_transposed() ? 1 : 0;
         g.B = a.qkv + h; g.b_mn_major = 1; g.ldb = 3 * h; g.b_s1 = hd; g.b_s2 = (long long)s * 3 * h;
         g.C = ws.dqkv; g.ldc = 3 * h; g.c_s1 = hd; g.c_s2 = (long long)s * 3 * h;
         g.alpha = scale;
