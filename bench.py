@@ -369,6 +369,8 @@ def main():
                                f"b={m['batch']}/GPU) planned offload at {a.gpu_mem_gib} GiB GPU budget",
                    "global_batch": m["batch"] * world, "seq_len": m["seq_len"], "parallelism": f"dp{world}",
                    "strategy": [st["c_hat"], st["p_hat"], st["o_hat"]],
+                   "planner": ("hetsim::dp::solve (per-rank sharded optimizer model)" if world > 1
+                               else "hetsim::solve (reference Eq.6)"),
                    "l2": "no flush needed: per-step working set (weights, activations, optimizer state) is "
                          "tens of GB >> 126 MB L2"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": 2 * T * 4, "d2h_bytes_per_step": 4},

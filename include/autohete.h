@@ -192,6 +192,12 @@ typedef struct ah_trainer_config {
      * !force_collectives => no NCCL. nccl_id: ncclUniqueId from ah_dp_unique_id on rank 0. */
     int32_t dp_rank, dp_size, force_collectives;
     uint8_t nccl_id[128];
+    /* dp_size > 1 and dp_aware_plan: plan with the data-parallel extension hetsim::dp::solve
+     * (include/hetsim/dp_planner.hpp: per-rank sharded optimizer memory and shard copy /
+     * optimizer times; collective_bw bytes/s bounds the block times, <= 0 = not modelled)
+     * instead of the single-GPU reference solve. */
+    int32_t dp_aware_plan;
+    double collective_bw;
 } ah_trainer_config;
 
 /* ncclGetUniqueId into out[128] (rank 0; broadcast it to the other ranks). */

@@ -30,6 +30,12 @@ int64_t ah_hetsim_block_param_count(int64_t hidden_size);
  * Returns the JSON length + 1 on success (call with out=NULL to size), < 0 on error. */
 int64_t ah_hetsim_plan_json(const char* config_text, char* out, size_t cap);
 
+/* Data-parallel extension (hetsim/dp_planner.hpp, not in the reference): plan for dp_size ranks
+ * with per-rank sharded optimizer state; collective_gbps <= 0 leaves collectives unmodelled.
+ * dp_size == 1 returns exactly ah_hetsim_plan_json's document. */
+int64_t ah_hetsim_plan_dp_json(const char* config_text, int32_t dp_size, double collective_gbps, char* out,
+                               size_t cap);
+
 /* `hetsim simulate CONFIG` (hetsim_main.cpp:132-201): plan (or use the given strategy when
  * c_hat >= 0), run(n_iters, priority) and write the Chrome trace (simulator.cpp:598-613). */
 int64_t ah_hetsim_simulate_trace(const char* config_text, int32_t c_hat, int32_t p_hat, int32_t o_hat,

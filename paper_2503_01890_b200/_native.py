@@ -131,6 +131,7 @@ class TrainerConfig(C.Structure):
         ("adam", AdamHParams), ("seed", C.c_uint64), ("cpu_threads", C.c_int32),
         ("dp_rank", C.c_int32), ("dp_size", C.c_int32), ("force_collectives", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
+        ("dp_aware_plan", C.c_int32), ("collective_bw", C.c_double),
     ]
 
 

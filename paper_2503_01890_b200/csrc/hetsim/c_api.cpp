@@ -8,6 +8,7 @@
 #include "hetsim/config.hpp"
 #include "hetsim/plan_io.hpp"
 #include "hetsim/planner.hpp"
+#include "hetsim/dp_planner.hpp"
 #include "hetsim/simulator.hpp"
 
 namespace {
@@ -63,6 +64,31 @@ int64_t ah_hetsim_plan_json(const char* text, char* out, size_t cap) {
         const hetsim::PlanResult r = hetsim::solve(req);
         hetsim::PlanDocument doc;
         doc.strategy = hetsim::fine_tune_prefetch(prof, r.strategy, cfg.hardware);
+        doc.cost = r.cost;
+        doc.gpu_margin = cfg.hardware.gpu_mem - r.cost.peak_gpu;
+        doc.cpu_margin = cfg.hardware.cpu_mem - r.cost.cpu_bytes;
+        doc.feasible_count = r.feasible_count;
+        std::ostringstream s;
+        hetsim::write_plan_json(s, doc);
+        return emit(s.str(), out, cap);
+    });
+}
+
+int64_t ah_hetsim_plan_dp_json(const char* text, int32_t dp_size, double collective_gbps, char* out, size_t cap) {
+    return guard([&]() -> int64_t {
+        const hetsim::RunConfig cfg = hetsim::parse_config(text ? text : "", "<memory>");
+        const hetsim::ModelProfile prof = hetsim::build_profile(cfg.model, cfg.hardware, cfg.overrides);
+        hetsim::PlanRequest req;
+        req.profile = prof;
+        req.hardware = cfg.hardware;
+        hetsim::dp::DpSpec dp;
+        dp.dp_size = dp_size;
+        dp.collective_bandwidth = collective_gbps * 1e9;
+        const hetsim::PlanResult r = hetsim::dp::solve(req, dp);
+        hetsim::PlanDocument doc;
+        hetsim::HardwareSpec hw_sim = cfg.hardware;
+        hw_sim.gpu_mem = hetsim::dp::simulator_gpu_budget(prof, r.strategy, cfg.hardware.gpu_mem, dp);
+        doc.strategy = hetsim::fine_tune_prefetch(hetsim::dp::rank_profile(prof, cfg.hardware, dp), r.strategy, hw_sim);
         doc.cost = r.cost;
         doc.gpu_margin = cfg.hardware.gpu_mem - r.cost.peak_gpu;
         doc.cpu_margin = cfg.hardware.cpu_mem - r.cost.cpu_bytes;

@@ -1,5 +1,6 @@
 // B200 executor of the planned AutoHete iteration (see executor.h).
 #include "executor.h"
+#include "hetsim/dp_planner.hpp"
 
 #include <algorithm>
 #include <chrono>
@@ -174,6 +175,8 @@ Trainer::~Trainer() {
 // ---------------------------------------------------------------------------------------
 void Trainer::plan(const ah_trainer_config& cfg) {
     const size_t T = d_.T(), h = d_.h;
+    dp_spec_.dp_size = dp_size_;
+    dp_spec_.collective_bandwidth = cfg.collective_bw;
     hetsim::ModelSpec spec;
     spec.num_blocks = d_.L;
     spec.hidden_size = d_.h;
@@ -204,11 +207,23 @@ void Trainer::plan(const ah_trainer_config& cfg) {
         if (cfg.prefetch_lookahead)
             for (int i = 0; i < L; ++i) strategy_.prefetch_lookahead[(size_t)i] = cfg.prefetch_lookahead[i];
         strategy_.validate(L);
+    } else if (dp_size_ > 1 && cfg.dp_aware_plan) {  // data-parallel extension (dp_planner.hpp)
+        hetsim::PlanRequest req;
+        req.profile = profile_;
+        req.hardware = hw_;
+        strategy_ = hetsim::dp::solve(req, dp_spec_).strategy;
     } else {
         hetsim::PlanRequest req;
         req.profile = profile_;
         req.hardware = hw_;
         strategy_ = hetsim::solve(req).strategy;
+    }
+    if (dp_size_ > 1 && cfg.dp_aware_plan) {
+        // schedule on the per-rank durations; the simulator's (unsharded) memory model gets the
+        // budget that admits the realised per-rank footprint
+        const hetsim::ModelProfile full = profile_;
+        profile_ = hetsim::dp::rank_profile(full, hw_, dp_spec_);
+        hw_.gpu_mem = hetsim::dp::simulator_gpu_budget(full, strategy_, hw_.gpu_mem, dp_spec_);
     }
     if (cfg.fine_tune) strategy_ = hetsim::fine_tune_prefetch(profile_, strategy_, hw_);
     sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
@@ -886,7 +901,7 @@ void Trainer::stats(ah_trainer_stats* s) {
     s->activation_coef = (double)profile_.block.m_a / (double)profile_.block.m_a_in;
     s->m_p = profile_.block.m_p;
     s->m_gc = profile_.m_gc;
-    s->modeled_peak_bytes = hetsim::peak_gpu_mem(profile_, strategy_);
+    s->modeled_peak_bytes = hetsim::dp::peak_gpu_mem(profile_, strategy_, dp_spec_);  // Eq.(1), per rank under DP
     s->simulated_peak_bytes = sim_.peak_gpu;
     uint64_t hw = 0;
     cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hw);

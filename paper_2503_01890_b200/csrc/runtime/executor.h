@@ -22,6 +22,7 @@
 
 #include "autohete.h"
 #include "gpt_model.h"
+#include "hetsim/dp_planner.hpp"
 #include "hetsim/planner.hpp"
 #include "hetsim/simulator.hpp"
 
@@ -150,6 +151,7 @@ private:
     hetsim::ModelProfile profile_;
     hetsim::HardwareSpec hw_;
     hetsim::Strategy strategy_;
+    hetsim::dp::DpSpec dp_spec_;
     hetsim::SimResult sim_;
     bool ps_ = true;
     ah_adam_hparams adam_{};

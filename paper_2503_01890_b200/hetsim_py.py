@@ -18,6 +18,8 @@ def lib():
         _lib.ah_hetsim_block_param_count.restype = C.c_int64
         _lib.ah_hetsim_plan_json.argtypes = [C.c_char_p, C.c_char_p, C.c_size_t]
         _lib.ah_hetsim_plan_json.restype = C.c_int64
+        _lib.ah_hetsim_plan_dp_json.argtypes = [C.c_char_p, C.c_int32, C.c_double, C.c_char_p, C.c_size_t]
+        _lib.ah_hetsim_plan_dp_json.restype = C.c_int64
         _lib.ah_hetsim_simulate_trace.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                                   C.c_char_p, C.c_size_t]
         _lib.ah_hetsim_simulate_trace.restype = C.c_int64
@@ -39,6 +41,11 @@ def block_param_count(h: int) -> int:
 
 def plan_json(config_text: str) -> str:
     return _text(lib().ah_hetsim_plan_json, config_text.encode())
+
+
+def plan_dp_json(config_text: str, dp_size: int, collective_gbps: float = 0.0) -> str:
+    """Data-parallel planner extension (hetsim/dp_planner.hpp): per-rank sharded optimizer."""
+    return _text(lib().ah_hetsim_plan_dp_json, config_text.encode(), int(dp_size), float(collective_gbps))
 
 
 def simulate_trace(config_text: str, strategy=(-1, -1, -1), n_iters=2, priority=True) -> str:

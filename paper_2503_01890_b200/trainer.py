@@ -45,6 +45,9 @@ class PlanConfig:
     cpu_adam_rate: float = 1.0e9
     gpu_adam_rate: float = 2.0e11
     bwd_fwd_ratio: float = 2.0
+    # data parallel: plan with the per-rank sharded model (hetsim::dp::solve) when dp_size > 1
+    dp_aware: bool = True
+    collective_bw: float = 0.0  # bytes/s of one rank's all-gather / reduce-scatter (0: not modelled)
 
 
 @dataclasses.dataclass
@@ -83,6 +86,7 @@ class Trainer:
         cfg.seed = seed
         cfg.cpu_threads = cpu_threads
         cfg.dp_rank, cfg.dp_size, cfg.force_collectives = dp_rank, dp_size, int(force_collectives)
+        cfg.dp_aware_plan, cfg.collective_bw = int(plan.dp_aware), float(plan.collective_bw)
         if dp_size > 1 or force_collectives:
             nid = nccl_id if nccl_id is not None else N.dp_unique_id()
             C.memmove(cfg.nccl_id, nid, 128)
