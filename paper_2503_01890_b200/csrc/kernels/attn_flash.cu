@@ -468,9 +468,13 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll
                     for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
                 }
-                float cm = v[0];
+                float mx[8];  // 8 independent chains (dependent-latency bound otherwise)
 #pragma unroll
-                for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
+                for (int i = 0; i < 8; ++i) mx[i] = v[i];
+#pragma unroll
+                for (int i = 8; i < 64; ++i) mx[i & 7] = fmaxf(mx[i & 7], v[i]);
+                const float cm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
                 xmax[(st * 2 + half) * 128 + r] = cm;
                 fence_before();
                 // both halves have their scores in registers past this barrier: P may overwrite S
@@ -490,14 +494,14 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                 }
                 const float mb = m_used * sl2;
                 float w[32];  // packed bf16 pairs, bit-cast to float for tcgen05.st
-                float add = 0.f;
+                float ad[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial sums
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
-                    add += p0 + p1;
+                    ad[i & 3] += p0 + p1;
                     w[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
                 }
-                l += add;
+                l += (ad[0] + ad[1]) + (ad[2] + ad[3]);
                 if (__any_sync(0xffffffffu, rescale)) {  // O += P V of tile g-1 must have landed
                     mbar_wait(smem_u32(pv_done), (g - 1) & 1);
                     fence_after();
