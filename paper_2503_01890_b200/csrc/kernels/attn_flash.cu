@@ -313,7 +313,8 @@ struct FwdItems {
     }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int kParts>
+__global__ void __launch_bounds__((4 + 4 * kParts) * 32, 1)
 flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                     const __grid_constant__ CUtensorMap tmV, const FwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -334,8 +335,10 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint64_t* pv_done = bar + 17;
     uint64_t* o_full = bar + 18;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 20);
-    float* xmax = reinterpret_cast<float*>(bar + 22);  // [2 parity][2 halves][128 rows]
-    float* xsum = xmax + 2 * 2 * 128;                  // [2 halves][128 rows]
+    constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
+    constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
+    float* xmax = reinterpret_cast<float*>(bar + 22);  // [2 parity][kParts][128 rows]
+    float* xsum = xmax + 2 * kParts * 128;             // [kParts][128 rows]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     FwdItems items{A.s / kT, A.nh, A.B, (A.s / kT) * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
@@ -352,9 +355,9 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             mbar_init(smem_u32(&v_full[i]), 1);
             mbar_init(smem_u32(&v_empty[i]), 1);
             mbar_init(smem_u32(&s_full[i]), 1);
-            mbar_init(smem_u32(&s_free[i]), 8);
+            mbar_init(smem_u32(&s_free[i]), kSoft);
         }
-        mbar_init(smem_u32(p_full), 8);
+        mbar_init(smem_u32(p_full), kSoft);
         mbar_init(smem_u32(pv_done), 1);
         mbar_init(smem_u32(o_full), 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -446,10 +449,10 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             }
         }
     } else if (warp >= 4) {  // ===== online softmax / epilogue =====
-        const int half = (warp - 4) >> 2, quarter = warp & 3;
+        const int part = (warp - 4) >> 2, quarter = warp & 3;  // keys / O columns [kC * part, kC * part + kC)
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = uint32_t(quarter * 32) << 16;
-        const int pair_bar = 1 + quarter;  // named barrier of warps (quarter, quarter + 4)
+        const int quad_bar = 1 + quarter;  // named barrier of the kParts warps of this row quarter
         const float sl2 = A.sl2;
         uint32_t g = 0;
         for (int it = 0; it < n_items; ++it) {
@@ -461,27 +464,32 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                 const int st = g & 1;
                 mbar_wait(smem_u32(&s_full[st]), (g >> 1) & 1);
                 fence_after();
-                float v[64];
-                ld64(tmem + lane_base + st * 128 + half * 64, v);
+                float v[kC];
+                if constexpr (kC == 64)
+                    ld64(tmem + lane_base + st * 128 + part * kC, *reinterpret_cast<float(*)[64]>(v));
+                else
+                    ld32(tmem + lane_base + st * 128 + part * kC, *reinterpret_cast<float(*)[32]>(v));
                 if (j == qt) {  // diagonal tile: keys > q are masked
-                    const int lim = q - j * kT - half * 64;
+                    const int lim = q - j * kT - part * kC;
 #pragma unroll
-                    for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
+                    for (int i = 0; i < kC; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
                 }
-                float mx[8];  // 8 independent chains (dependent-latency bound otherwise)
+                float mx[8];  // 8 independent chains
 #pragma unroll
                 for (int i = 0; i < 8; ++i) mx[i] = v[i];
 #pragma unroll
-                for (int i = 8; i < 64; ++i) mx[i & 7] = fmaxf(mx[i & 7], v[i]);
+                for (int i = 8; i < kC; ++i) mx[i & 7] = fmaxf(mx[i & 7], v[i]);
                 const float cm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                        fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-                xmax[(st * 2 + half) * 128 + r] = cm;
+                xmax[(st * kParts + part) * 128 + r] = cm;
                 fence_before();
-                // both halves have their scores in registers past this barrier: P may overwrite S
-                asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
+                // every slice has its scores in registers past this barrier: P may overwrite S
+                asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");
                 fence_after();
                 if (lane == 0) mbar_arrive(smem_u32(&s_free[st]));
-                const float mt = fmaxf(cm, xmax[(st * 2 + (half ^ 1)) * 128 + r]);  // finite: key 0 <= q
+                float mt = xmax[(st * kParts) * 128 + r];  // finite: key 0 <= q
+#pragma unroll
+                for (int pp = 1; pp < kParts; ++pp) mt = fmaxf(mt, xmax[(st * kParts + pp) * 128 + r]);
                 float alpha = 1.f;
                 bool rescale = false;
                 if (m_used == -INFINITY) {
@@ -493,10 +501,10 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                     rescale = true;
                 }
                 const float mb = m_used * sl2;
-                float w[32];  // packed bf16 pairs, bit-cast to float for tcgen05.st
-                float ad[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent partial sums
+                float w[kC / 2];  // packed bf16 pairs, bit-cast to float for tcgen05.st
+                float ad[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
+                for (int i = 0; i < kC / 2; ++i) {
                     const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
                     ad[i & 3] += p0 + p1;
                     w[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
@@ -506,33 +514,39 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                     mbar_wait(smem_u32(pv_done), (g - 1) & 1);
                     fence_after();
 #pragma unroll 1
-                    for (int c = 0; c < 2; ++c) {
+                    for (int c = 0; c < kC / 32; ++c) {
                         float o[32];
-                        const uint32_t ta = tmem + lane_base + 256 + half * 64 + c * 32;
+                        const uint32_t ta = tmem + lane_base + 256 + part * kC + c * 32;
                         ld32(ta, o);
 #pragma unroll
                         for (int i = 0; i < 32; ++i) o[i] *= alpha;
                         st32(ta, o);
                     }
                 }
-                st32(tmem + lane_base + st * 128 + half * 32, w);  // P_j -> first 64 columns of its S buffer
+                // P_j -> first 64 columns of its S buffer (this slice's kC keys = kC / 2 columns)
+                if constexpr (kC == 64)
+                    st32(tmem + lane_base + st * 128 + part * (kC / 2), *reinterpret_cast<float(*)[32]>(w));
+                else
+                    st16(tmem + lane_base + st * 128 + part * (kC / 2), *reinterpret_cast<float(*)[16]>(w));
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(p_full));
             }
-            xsum[half * 128 + r] = l;
-            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-            const float lt = l + xsum[(half ^ 1) * 128 + r];
-            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");  // xsum reused by the next item
+            xsum[part * 128 + r] = l;
+            asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");
+            float lt = xsum[r];
+#pragma unroll
+            for (int pp = 1; pp < kParts; ++pp) lt += xsum[pp * 128 + r];
+            asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");  // xsum reused next item
             const float inv = 1.f / lt;
-            if (half == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
+            if (part == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
             mbar_wait(smem_u32(o_full), it & 1);
             fence_after();
-            uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + half * 64;
+            uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + part * kC;
 #pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
+            for (int c = 0; c < kC / 32; ++c) {
                 float v[32];
-                ld32(tmem + lane_base + 256 + half * 64 + c * 32, v);
+                ld32(tmem + lane_base + 256 + part * kC + c * 32, v);
                 uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8)
@@ -1446,12 +1460,27 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
         flash_fwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, a);
         return launched(1);
     }
-    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 6 * 128 * 4;
-    static bool cfg2 = false;
-    cudaError_t e = set_smem(flash_fwd_pk_kernel, smem, cfg2);
-    if (e != cudaSuccess) return e;
+    // default: 8 softmax warps (64 keys each, 63 us at B=8 s=1024 16 heads); AH_FLASH_FWD=pk4:
+    // 16 softmax warps (32 keys each, 66 us) — the softmax warps are not the limiter
+    static const int parts = [] {
+        const char* e = std::getenv("AH_FLASH_FWD");
+        return (e && e[0] == 'p' && e[1] == 'k' && e[2] == '4') ? 4 : 2;
+    }();
     const int items = (s / kT) * nh * B;
-    flash_fwd_pk_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, a);
+    const int grid = items < kNumSMs ? items : kNumSMs;
+    if (parts == 2) {
+        const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 6 * 128 * 4;
+        static bool cfg2 = false;
+        cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
+        if (e != cudaSuccess) return e;
+        flash_fwd_pk_kernel<2><<<grid, (4 + 8) * 32, smem, st>>>(mq, mk, mv, a);
+        return launched(1);
+    }
+    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 12 * 128 * 4;
+    static bool cfg4 = false;
+    cudaError_t e = set_smem(flash_fwd_pk_kernel<4>, smem, cfg4);
+    if (e != cudaSuccess) return e;
+    flash_fwd_pk_kernel<4><<<grid, (4 + 16) * 32, smem, st>>>(mq, mk, mv, a);
     return launched(1);
 }
 
