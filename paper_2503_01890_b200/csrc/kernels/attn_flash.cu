@@ -337,8 +337,9 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 20);
     constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
     constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
-    float* xmax = reinterpret_cast<float*>(bar + 22);  // [2 parity][kParts][128 rows]
-    float* xsum = xmax + 2 * kParts * 128;             // [kParts][128 rows]
+    // statically shared (not carved from the aligned dynamic block) so the compiler emits LDS/STS
+    __shared__ float xmax[2 * kParts * 128];  // [2 parity][kParts][128 rows]
+    __shared__ float xsum[kParts * 128];      // [kParts][128 rows]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     FwdItems items{A.s / kT, A.nh, A.B, (A.s / kT) * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
@@ -1469,14 +1470,14 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     const int items = (s / kT) * nh * B;
     const int grid = items < kNumSMs ? items : kNumSMs;
     if (parts == 2) {
-        const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 6 * 128 * 4;
+        const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8;
         static bool cfg2 = false;
         cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
         if (e != cudaSuccess) return e;
         flash_fwd_pk_kernel<2><<<grid, (4 + 8) * 32, smem, st>>>(mq, mk, mv, a);
         return launched(1);
     }
-    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8 + 12 * 128 * 4;
+    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8;
     static bool cfg4 = false;
     cudaError_t e = set_smem(flash_fwd_pk_kernel<4>, smem, cfg4);
     if (e != cudaSuccess) return e;
