@@ -61,6 +61,24 @@ __device__ __forceinline__ float4 cta_sum4(float4 v, float4* red, int& slot) {
     return t;
 }
 
+// Two-value variant (the forward's per-row-pair mean / variance): half the shuffles.
+__device__ __forceinline__ float2 cta_sum2v(float a, float b, float4* red, int& slot) {
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int nw = blockDim.x >> 5, w = threadIdx.x >> 5;
+    float2* r = reinterpret_cast<float2*>(red + slot * 32);
+    if ((threadIdx.x & 31) == 0) r[w] = make_float2(a, b);
+    __syncthreads();
+    float2 t = r[0];
+    for (int q = 1; q < nw; ++q) {
+        const float2 u = r[q];
+        t.x += u.x;
+        t.y += u.y;
+    }
+    slot ^= 1;
+    return t;
+}
+
 // Two rows per iteration share each barrier, so the ring holds 3 iterations of rows.
 constexpr int kRing = 6;
 
@@ -154,7 +172,7 @@ __global__ void __launch_bounds__(768) ln_fwd_rows_kernel(const uint16_t* __rest
             sa += fa[i];
             sb += fb[i];
         }
-        const float4 m = cta_sum4(make_float4(sa, sb, 0.f, 0.f), red, slot);
+        const float2 m = cta_sum2v(sa, sb, red, slot);
         if (threadIdx.x == 0) {  // both stages are free: refill them
             if (j + ring < n) issue(j + ring, st);
             if (j + 1 + ring < n) issue(j + 1 + ring, st + 1);
@@ -171,7 +189,7 @@ __global__ void __launch_bounds__(768) ln_fwd_rows_kernel(const uint16_t* __rest
             va += (fa[i] - mua) * (fa[i] - mua);
             vb += (fb[i] - mub) * (fb[i] - mub);
         }
-        const float4 v = cta_sum4(make_float4(va, vb, 0.f, 0.f), red, slot);
+        const float2 v = cta_sum2v(va, vb, red, slot);
         const float rsa = rsqrtf(v.x * inv_h + kLnEps), rsb = rsqrtf(v.y * inv_h + kLnEps);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
