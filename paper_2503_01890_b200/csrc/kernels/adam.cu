@@ -370,7 +370,7 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
             const char* e = std::getenv("AH_ADAM_KERNEL");
             return !(e && e[0] == 'v');  // AH_ADAM_KERNEL=vec selects the register-streaming kernel
         }();
-        if (n_vec && use_tma) {
+        if (n_vec && use_tma && a.max_ctas <= 0) {
             const size_t tiles = (n_vec * 8 + kTile - 1) / kTile;
             const int grid = (int)(tiles < (size_t)kNumSMs ? tiles : (size_t)kNumSMs);
             static bool attr = [] {
@@ -391,7 +391,8 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
             else
                 adam_tma_kernel<false, false><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
         } else if (n_vec) {
-            const int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
+            int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
+            if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
             if (a.p_bf16 && a.stats)
                 adam_vec_kernel<true, true><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
             else if (a.p_bf16)

@@ -19,6 +19,8 @@ struct AdamArgs {
     float inv_scale = 1.f;
     const int* skip = nullptr;   // nullable device flag
     float* stats = nullptr;      // nullable device [sumsq(float), nonfinite(uint32)]
+    int max_ctas = 0;            // > 0: register-streaming kernel on at most this many CTAs (runs beside
+                                 // a persistent GEMM on a side stream instead of taking every SM)
 };
 
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);

@@ -111,6 +111,8 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     {
         const char* e = std::getenv("AH_PREFETCH_WEIGHTS");
         prefetch_mat_ = !(e && e[0] == '0');
+        const char* o = std::getenv("AH_OPT_SIDE_CTAS");  // experiment knob, off by default
+        opt_side_ctas_ = o ? std::atoi(o) : 0;
     }
     plan(cfg);
     allocate_and_init();
@@ -654,8 +656,17 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             AdamArgs aa = dp_ ? adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf + off, nullptr, shard_)
                               : adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf, nullptr, mp);
             aa.inv_scale = 1.f / (float)dp_size_;
-            check(launch_adam(aa, st), "adam");
-            free_wbuf();
+            if (opt_side_ctas_ > 0) {  // experiment: the update overlaps the next backward on the side stream
+                side_after_compute();
+                aa.max_ctas = opt_side_ctas_;
+                check(launch_adam(aa, s_side_), "adam");
+                check(cudaFreeAsync(b.wbuf, s_side_), "free wbuf");
+                b.wbuf = nullptr;
+                op.done_on_side = true;
+            } else {
+                check(launch_adam(aa, st), "adam");
+                free_wbuf();
+            }
             break;
         }
         default:
