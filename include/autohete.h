@@ -198,12 +198,19 @@ typedef struct ah_trainer_config {
      * instead of the single-GPU reference solve. */
     int32_t dp_aware_plan;
     double collective_bw;
+    /* non-null: exchange with these in-process ranks through an ah_dp_loopback_create
+     * communicator instead of NCCL (all ranks on one GPU; validation of the DP path). */
+    void* loopback_comm;
 } ah_trainer_config;
 
 /* ncclGetUniqueId into out[128] (rank 0; broadcast it to the other ranks). */
 int ah_dp_unique_id(uint8_t* out);
 /* Shard of a flat block vector of n elements owned by `rank` (16-byte aligned shards):
  * elements [*offset, *offset + *len) of the padded vector of dp_size * (*shard) elements. */
+/* In-process loopback communicator for nranks trainers sharing one GPU (same in-place
+ * collective semantics as the NCCL path; device copies + a fixed-order sum kernel). */
+int ah_dp_loopback_create(int32_t nranks, void** comm);
+int ah_dp_loopback_destroy(void* comm);
 int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard);
 
 typedef struct ah_trainer_stats {

@@ -132,6 +132,7 @@ class TrainerConfig(C.Structure):
         ("dp_rank", C.c_int32), ("dp_size", C.c_int32), ("force_collectives", C.c_int32),
         ("nccl_id", C.c_uint8 * 128),
         ("dp_aware_plan", C.c_int32), ("collective_bw", C.c_double),
+        ("loopback_comm", C.c_void_p),
     ]
 
 
@@ -179,6 +180,8 @@ _EXTRA_SIGS.update({
 
 _EXTRA_SIGS.update({
     "ah_dp_unique_id": ([C.c_void_p], C.c_int),
+    "ah_dp_loopback_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
+    "ah_dp_loopback_destroy": ([C.c_void_p], C.c_int),
     "ah_dp_shard": ([C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                      C.POINTER(C.c_int64)], C.c_int),
 })

@@ -139,6 +139,8 @@ int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out) {
 
 #include <nccl.h>
 
+#include "../runtime/loopback_comm.h"
+
 extern "C" {
 
 int ah_dp_unique_id(uint8_t* out) {
@@ -147,6 +149,21 @@ int ah_dp_unique_id(uint8_t* out) {
     const ncclResult_t r = ncclGetUniqueId(&id);
     if (r != ncclSuccess) return ah::set_error(AH_ERR_NCCL, std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
     std::memcpy(out, &id, sizeof(id));
+    return AH_OK;
+}
+
+int ah_dp_loopback_create(int32_t nranks, void** comm) {
+    if (!comm) return ah::set_error(AH_ERR_INVALID, "ah_dp_loopback_create: null out");
+    try {
+        *comm = new ah::LoopbackComm(nranks);
+    } catch (const std::exception& e) {
+        return ah::set_error(AH_ERR_INVALID, std::string("ah_dp_loopback_create: ") + e.what());
+    }
+    return AH_OK;
+}
+
+int ah_dp_loopback_destroy(void* comm) {
+    delete static_cast<ah::LoopbackComm*>(comm);
     return AH_OK;
 }
 

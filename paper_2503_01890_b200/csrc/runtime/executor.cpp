@@ -1,6 +1,7 @@
 // B200 executor of the planned AutoHete iteration (see executor.h).
 #include "executor.h"
 #include "hetsim/dp_planner.hpp"
+#include "loopback_comm.h"
 
 #include <algorithm>
 #include <chrono>
@@ -88,10 +89,14 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     dp_size_ = cfg.dp_size < 1 ? 1 : cfg.dp_size;
     dp_ = dp_size_ > 1 || cfg.force_collectives;
     if (dp_rank_ < 0 || dp_rank_ >= dp_size_) throw std::invalid_argument("trainer: dp_rank out of range");
+    loop_ = static_cast<LoopbackComm*>(cfg.loopback_comm);
+    if (loop_ && loop_->size() != dp_size_) throw std::invalid_argument("trainer: loopback comm size != dp_size");
     if (dp_) {
         shard_ = round_up((d_.m_p() + dp_size_ - 1) / dp_size_, 8);
         const size_t off = shard_ * (size_t)dp_rank_;
         my_len_ = off >= d_.m_p() ? 0 : std::min(shard_, d_.m_p() - off);
+    }
+    if (dp_ && !loop_) {
         ncclUniqueId id;
         static_assert(sizeof(id) == 128, "ncclUniqueId size");
         std::memcpy(&id, cfg.nccl_id, sizeof(id));
@@ -750,23 +755,28 @@ void Trainer::prefetch_weights(const Iter& it, size_t idx) {
 }
 
 void Trainer::dp_gather(uint16_t* wbuf, cudaStream_t st) {
+    if (loop_) return check(loop_->call(dp_rank_, LoopbackComm::kAllGatherBf16, wbuf, shard_, st), "loopback all-gather");
     const ncclResult_t r = ncclAllGather(wbuf + shard_ * (size_t)dp_rank_, wbuf, shard_, ncclBfloat16,
                                          static_cast<ncclComm_t>(comm_), st);
     if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
 }
 
 void Trainer::dp_reduce_grads(uint16_t* wbuf, cudaStream_t st) {
+    if (loop_)
+        return check(loop_->call(dp_rank_, LoopbackComm::kReduceScatterBf16, wbuf, shard_, st), "loopback reduce-scatter");
     const ncclResult_t r = ncclReduceScatter(wbuf, wbuf + shard_ * (size_t)dp_rank_, shard_, ncclBfloat16, ncclSum,
                                              static_cast<ncclComm_t>(comm_), st);
     if (r != ncclSuccess) throw std::runtime_error(std::string("ncclReduceScatter: ") + ncclGetErrorString(r));
 }
 
 void Trainer::dp_allreduce_f32(float* p, size_t n, cudaStream_t st) {
+    if (loop_) return check(loop_->call(dp_rank_, LoopbackComm::kAllReduceF32, p, n, st), "loopback all-reduce");
     const ncclResult_t r = ncclAllReduce(p, p, n, ncclFloat32, ncclSum, static_cast<ncclComm_t>(comm_), st);
     if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }
 
 void Trainer::dp_allreduce_bf16(uint16_t* p, size_t n, cudaStream_t st) {
+    if (loop_) return check(loop_->call(dp_rank_, LoopbackComm::kAllReduceBf16, p, n, st), "loopback all-reduce");
     const ncclResult_t r = ncclAllReduce(p, p, n, ncclBfloat16, ncclSum, static_cast<ncclComm_t>(comm_), st);
     if (r != ncclSuccess) throw std::runtime_error(std::string("ncclAllReduce: ") + ncclGetErrorString(r));
 }

@@ -73,6 +73,7 @@ private:
     int device_ = 0;  // the caller's current device at construction; every lane thread binds to it
     bool dp_ = false;      // collectives on
     void* comm_ = nullptr; // ncclComm_t
+    class LoopbackComm* loop_ = nullptr;  // in-process ranks on one GPU instead of NCCL (not owned)
     size_t shard_ = 0;     // per-rank shard length of a block vector (elements, padded)
     size_t my_len_ = 0;    // valid elements of this rank's shard
     size_t full_len() const { return dp_ ? shard_ * (size_t)dp_size_ : d_.m_p(); }

@@ -62,7 +62,7 @@ class AdamConfig:
 class Trainer:
     def __init__(self, model: ModelConfig, plan: PlanConfig | None = None, adam: AdamConfig | None = None,
                  seed: int = 1234, cpu_threads: int = 0, dp_rank: int = 0, dp_size: int = 1,
-                 nccl_id: bytes | None = None, force_collectives: bool = False):
+                 nccl_id: bytes | None = None, force_collectives: bool = False, loopback=None):
         """dp_size > 1: data parallel over NCCL; every rank passes the same nccl_id (from
         _native.dp_unique_id() on rank 0) and the same seed / plan."""
         plan = plan or PlanConfig()
@@ -87,7 +87,9 @@ class Trainer:
         cfg.cpu_threads = cpu_threads
         cfg.dp_rank, cfg.dp_size, cfg.force_collectives = dp_rank, dp_size, int(force_collectives)
         cfg.dp_aware_plan, cfg.collective_bw = int(plan.dp_aware), float(plan.collective_bw)
-        if dp_size > 1 or force_collectives:
+        if loopback is not None:  # in-process ranks on one GPU (validation of the DP path)
+            cfg.loopback_comm = loopback.handle
+        elif dp_size > 1 or force_collectives:
             nid = nccl_id if nccl_id is not None else N.dp_unique_id()
             C.memmove(cfg.nccl_id, nid, 128)
         self._h = C.c_void_p()
@@ -173,6 +175,19 @@ class Trainer:
         buf = C.create_string_buffer(max(n, 1) + 4096)
         N.check(min(0, N.lib().ah_trainer_trace(self._h, buf, len(buf))), "ah_trainer_trace")
         return json.loads(buf.value.decode())
+
+
+class LoopbackComm:
+    """ah_dp_loopback_create: an in-process communicator for `nranks` Trainers on one GPU."""
+
+    def __init__(self, nranks: int):
+        self.handle = C.c_void_p()
+        N.check(N.lib().ah_dp_loopback_create(nranks, C.byref(self.handle)), "ah_dp_loopback_create")
+
+    def close(self):
+        if self.handle:
+            N.lib().ah_dp_loopback_destroy(self.handle)
+            self.handle = C.c_void_p()
 
 
 def profile_hardware(model: ModelConfig, cpu_threads: int = 0) -> dict:
