@@ -358,15 +358,24 @@ ce_reg_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__
         m2 = bf16x2_max(bf16x2_max(m2, bf16x2_max(r[i].x, r[i].y)), bf16x2_max(r[i].z, r[i].w));
     float m = fmaxf(bf16_bits_to_f32(m2 & 0xffffu), bf16_bits_to_f32(m2 >> 16));
     float sum = 0.f;
-    if (m != -INFINITY) {
+    if (m != -INFINITY) {  // one exp per logit: e = exp(f - m_thread) replaces the logit in r (bf16)
 #pragma unroll
         for (int i = 0; i < kCeVec; ++i) {
             float f[8];
             unpack8(r[i], f);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) sum += __expf(f[e] - m);
+            for (int e = 0; e < 8; ++e) {
+                f[e] = __expf(f[e] - m);
+                sum += f[e];
+            }
+            r[i] = make_uint4(pack_bf16x2_rn(f[0], f[1]), pack_bf16x2_rn(f[2], f[3]), pack_bf16x2_rn(f[4], f[5]),
+                              pack_bf16x2_rn(f[6], f[7]));
         }
+    } else {  // only padding in this thread: exp(-inf) = 0
+#pragma unroll
+        for (int i = 0; i < kCeVec; ++i) r[i] = make_uint4(0u, 0u, 0u, 0u);
     }
+    const float m_thread = m;
     // block combine of (m, sum) pairs
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -386,7 +395,8 @@ ce_reg_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__
     for (int q = 0; q < kCeThreads / 32; ++q)
         if (red_m[q] != -INFINITY) S += red_s[q] * __expf(red_m[q] - M);
     if (threadIdx.x == 0) loss[row] = M + __logf(S) - tl;
-    const float inv = 1.f / S;
+    // softmax = e * exp(m_thread - M) / S (e held in bf16: the gradient is stored in bf16 anyway)
+    const float inv = m_thread == -INFINITY ? 0.f : __expf(m_thread - M) / S;
 #pragma unroll
     for (int i = 0; i < kCeVec; ++i) {
         const int idx = threadIdx.x + i * kCeThreads;
@@ -397,9 +407,9 @@ ce_reg_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__
         uint32_t o[4];
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
-            const float d0 = (__expf(f[e] - M) * inv - (c0 + e == t ? 1.f : 0.f)) * dscale;
-            const float d1 = (__expf(f[e + 1] - M) * inv - (c0 + e + 1 == t ? 1.f : 0.f)) * dscale;
-            o[e >> 1] = pack_bf16x2(d0, d1);
+            const float d0 = (f[e] * inv - (c0 + e == t ? 1.f : 0.f)) * dscale;
+            const float d1 = (f[e + 1] * inv - (c0 + e + 1 == t ? 1.f : 0.f)) * dscale;
+            o[e >> 1] = pack_bf16x2_rn(d0, d1);
         }
         *reinterpret_cast<uint4*>(lr + (size_t)c0) = make_uint4(o[0], o[1], o[2], o[3]);
     }
