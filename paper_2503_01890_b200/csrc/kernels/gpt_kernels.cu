@@ -638,20 +638,43 @@ __global__ void __launch_bounds__(1024) token_index_kernel(const int* __restrict
             __syncthreads();
         }
     }
-    for (int i = threadIdx.x; i < T; i += blockDim.x)
-        flag[i] = (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+    // distinct-token compaction: each thread owns a contiguous chunk of the sorted keys, counts
+    // the chunk's group starts, and a block-wide exclusive scan gives its output offset
+    const int chunk = (T + (int)blockDim.x - 1) / (int)blockDim.x;
+    const int i0 = min(T, (int)threadIdx.x * chunk), i1 = min(T, i0 + chunk);
+    int cnt = 0;
+    for (int i = i0; i < i1; ++i) cnt += (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
+    if (lane == 31) flag[wid] = incl;  // per-warp totals
     __syncthreads();
-    if (threadIdx.x == 0) {  // serial scan over T <= 16384 flags (tiny)
-        int u = 0;
-        for (int i = 0; i < T; ++i) {
-            if (flag[i]) {
-                uniq[u] = (int)(keys[i] >> 32);
-                offs[u] = i;
-                ++u;
-            }
+    if (wid == 0) {
+        const int nw = (int)blockDim.x >> 5;
+        int t = lane < nw ? flag[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, t, o);
+            if (lane >= o) t += y;
         }
-        offs[u] = T;
-        *n_uniq = u;
+        if (lane < nw) flag[32 + lane] = t - flag[lane];  // exclusive warp offsets
+        if (lane == nw - 1) flag[64] = t;                  // number of distinct tokens
+    }
+    __syncthreads();
+    int u = flag[32 + wid] + incl - cnt;
+    for (int i = i0; i < i1; ++i)
+        if (i == 0 || (keys[i] >> 32) != (keys[i - 1] >> 32)) {
+            uniq[u] = (int)(keys[i] >> 32);
+            offs[u] = i;
+            ++u;
+        }
+    if (threadIdx.x == 0) {
+        offs[flag[64]] = T;
+        *n_uniq = flag[64];
     }
     for (int i = threadIdx.x; i < T; i += blockDim.x) pos[i] = (int)(keys[i] & 0xffffffffu);
 }
