@@ -210,6 +210,55 @@ __global__ void __launch_bounds__(768) ln_fwd_rows_kernel(const uint16_t* __rest
     }
 }
 
+// Forward, warp per row with the whole row in registers (h = 256 * NC): all NC 16-byte loads
+// of a row are issued before any arithmetic, the two statistics are warp-shuffle reductions (no
+// CTA barrier), so ~6 rows per SM are in flight with no shared-memory staging at all.
+template <int NC>
+__global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const uint16_t* __restrict__ x, const uint16_t* __restrict__ g,
+                                                         const uint16_t* __restrict__ b, uint16_t* __restrict__ y,
+                                                         float* __restrict__ mean, float* __restrict__ rstd, int T) {
+    constexpr int h = NC * 256;
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= T) return;
+    const uint16_t* xr = x + (size_t)row * h + lane * 8;
+    uint4 w[NC];
+#pragma unroll
+    for (int k = 0; k < NC; ++k) w[k] = ld_stream_u4(xr + k * 256);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float f[8];
+        unpack8(w[k], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s += f[i];
+    }
+    const float mu = warp_sum(s) * (1.0f / h);
+    float v = 0.f;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float f[8];
+        unpack8(w[k], f);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v += (f[i] - mu) * (f[i] - mu);
+    }
+    const float rs = rsqrtf(warp_sum(v) * (1.0f / h) + kLnEps);
+    uint16_t* yr = y + (size_t)row * h + lane * 8;
+#pragma unroll
+    for (int k = 0; k < NC; ++k) {
+        float f[8], gg[8], bb[8];
+        unpack8(w[k], f);
+        unpack8(ldg16(g + k * 256 + lane * 8), gg);
+        unpack8(ldg16(b + k * 256 + lane * 8), bb);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) f[i] = (f[i] - mu) * rs * gg[i] + bb[i];
+        st_u4(yr + k * 256, pack8_rn(f));
+    }
+    if (lane == 0) {
+        mean[row] = mu;
+        rstd[row] = rs;
+    }
+}
+
 // One row of the backward, first half: xhat in place, row partial sums, column accumulators.
 template <bool kRes>
 struct BwdRow {
@@ -437,6 +486,13 @@ bool ln_rows_supported(int h) { return h % 256 == 0 && h / 8 <= 768; }
 cudaError_t ln_fwd_rows(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean,
                         float* rstd, int T, int h, cudaStream_t st) {
     if (T <= 0) return cudaSuccess;
+    switch (h) {  // register-resident warp-per-row forms for the common widths
+        case 768: ln_fwd_warp_kernel<3><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
+        case 1024: ln_fwd_warp_kernel<4><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
+        case 2048: ln_fwd_warp_kernel<8><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
+        case 4096: ln_fwd_warp_kernel<16><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
+        default: break;
+    }
     const int threads = h / 8;
     if (!aligned16(x) || !aligned16(y)) return cudaErrorMisalignedAddress;  // bulk copies need 16-B rows
     static bool attr = [] {
