@@ -211,8 +211,22 @@ __device__ __forceinline__ Tile decode_at(const Params& P, int z, int tm, int tn
 // takes CS consecutive M tiles; a rank past the last M tile computes an all-zero phantom tile
 // (TMA zero-fills, the epilogue masks rows >= M) so every CTA of a cluster runs the same
 // pipeline.
+// Causal K-range modes: tile cost grows (KUptoM) or shrinks (KFromM) with the M tile, so tiles
+// are enumerated heaviest M row first and dealt to CTAs in snake order (longest-processing-time
+// first); z / N vary fastest inside an M row.
+__device__ __forceinline__ bool causal_lpt(const Params& P) {
+    return P.causal == kCausalKUptoM || P.causal == kCausalKFromM;
+}
+
 template <int CS>
 __device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int crank) {
+    if (CS == 1 && causal_lpt(P)) {
+        const int per_m = P.tiles_n * P.batch1 * P.batch2;
+        const int r = ct / per_m, rest = ct - r * per_m;
+        const int tm = P.causal == kCausalKUptoM ? P.tiles_m - 1 - r : r;
+        const int z = rest / P.tiles_n;
+        return decode_at(P, z, tm, rest - z * P.tiles_n, BN);
+    }
     const int tmg = (P.tiles_m + CS - 1) / CS;
     const int per_z = tmg * P.tiles_n;
     const int z = ct / per_z;
@@ -231,6 +245,10 @@ __device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int cran
 template <int CS>
 __device__ __forceinline__ int num_segments(const Params& P) {
     const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
+    if (CS == 1 && causal_lpt(P)) {  // snake: round k takes k*ncl + (k even ? cid : ncl-1-cid)
+        const int full = P.num_tiles / ncl, rem = P.num_tiles - full * ncl;
+        return full + ((rem && ((full & 1) == 0 ? cid < rem : (ncl - 1 - cid) < rem)) ? 1 : 0);
+    }
     if (!P.sk) return cid < P.num_tiles ? (P.num_tiles - 1 - cid) / ncl + 1 : 0;
     const int waves = P.num_tiles / ncl, tail = P.num_tiles - waves * ncl;
     return waves + (cid < 2 * tail ? 1 : 0);
@@ -238,6 +256,12 @@ __device__ __forceinline__ int num_segments(const Params& P) {
 
 template <int CS>
 __device__ __forceinline__ Tile segment(const Params& P, int i, int BN, int crank) {
+    if (CS == 1 && causal_lpt(P)) {
+        const int ncl = gridDim.x, cid = blockIdx.x;
+        Tile T = decode<CS>(P, i * ncl + ((i & 1) == 0 ? cid : ncl - 1 - cid), BN, crank);
+        T.role = 0;
+        return T;
+    }
     if (!P.sk) {
         Tile T = decode<CS>(P, blockIdx.x / CS + i * (gridDim.x / CS), BN, crank);
         T.role = 0;
