@@ -346,7 +346,7 @@ def main():
     wi = max(1.0, st_t["window_iters"])
     copy_ms = st_t["h2d_busy_ms"] + st_t["d2h_busy_ms"]
     offload = {
-        "hidden_frac": (1.0 - st_t["offload_blocked_ms"] / copy_ms) if copy_ms > 0 else None,
+        "hidden_frac": max(0.0, 1.0 - st_t["offload_blocked_ms"] / copy_ms) if copy_ms > 0 else None,
         "compute_blocked_ms_per_step": st_t["offload_blocked_ms"] / wi,
         "h2d_ms_per_step": st_t["h2d_busy_ms"] / wi, "d2h_ms_per_step": st_t["d2h_busy_ms"] / wi,
         "compute_busy_ms_per_step": st_t["compute_busy_ms"] / wi,
@@ -403,6 +403,10 @@ def main():
         "model_flops_per_token": flops_per_token(m),
         "mfu_model": value / world * flops_per_token(m) / (bf16_peak * 1e12),
         "loss": loss,
+        # which lane bounds the step: the compute stream, or the host AdamW lane (the 10B and
+        # full-offload plans), in which case compute waits on CpuOptim and little can be "hidden"
+        "bound_by": ("cpu_optimizer_lane" if st["lane_busy_ms"][3] / max(1, a.steps + ke + a.warmup)
+                     >= 0.85 * ms_max / a.steps else "compute_lane"),
         "plan": {"strategy": [st["c_hat"], st["p_hat"], st["o_hat"]], "activation_coef": st["activation_coef"],
                  "modeled_peak_gib": st["modeled_peak_bytes"] / 2**30,
                  "simulated_peak_gib": st["simulated_peak_bytes"] / 2**30,
