@@ -333,8 +333,9 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint64_t* s_free = bar + 14;   // [2]
     uint64_t* p_full = bar + 16;
     uint64_t* pv_done = bar + 17;
-    uint64_t* o_full = bar + 18;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 20);
+    uint64_t* o_full = bar + 18;  // [2] O buffer of an item complete
+    uint64_t* o_free = bar + 20;  // [2] softmax warps have drained an O buffer
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 22);
     constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
     constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
     // statically shared (not carved from the aligned dynamic block) so the compiler emits LDS/STS
@@ -360,7 +361,10 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         }
         mbar_init(smem_u32(p_full), kSoft);
         mbar_init(smem_u32(pv_done), 1);
-        mbar_init(smem_u32(o_full), 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&o_full[i]), 1);
+            mbar_init(smem_u32(&o_free[i]), kSoft);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -372,7 +376,7 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = *tmem_holder;  // S/P[0] 0-127, S/P[1] 128-255, O 256-383
+    const uint32_t tmem = *tmem_holder;  // S/P[0] 0-127, S/P[1] 128-255, O[0] 256-383, O[1] 384-511
 
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
@@ -433,20 +437,22 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             for (int it = 0; it < n_items; ++it) {
                 int qt, head, b;
                 items.get(it, qt, head, b);
+                const uint32_t o_acc = tmem + 256 + (it & 1) * 128;  // O double-buffered across items
                 for (int j = 0; j <= qt; ++j, ++g) {
                     if (s_it < n_items) issue_next_S();  // scores of the next tile overlap softmax of this one
                     const int st = g & 1;
+                    if (j == 0 && it >= 2) mbar_wait(smem_u32(&o_free[it & 1]), ((it >> 1) & 1) ^ 1);
                     mbar_wait(smem_u32(p_full), g & 1);
                     mbar_wait(smem_u32(&v_full[st]), (g >> 1) & 1);
                     fence_after();
                     const uint32_t va = smem_u32(sV + st * kTile);
 #pragma unroll
                     for (int t = 0; t < 8; ++t)
-                        mma_f16_ts(tmem + 256, tmem + st * 128 + t * 8, mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
+                        mma_f16_ts(o_acc, tmem + st * 128 + t * 8, mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
                     commit(smem_u32(pv_done));
                     commit(smem_u32(&v_empty[st]));
                 }
-                commit(smem_u32(o_full));
+                commit(smem_u32(&o_full[it & 1]));
             }
         }
     } else if (warp >= 4) {  // ===== online softmax / epilogue =====
@@ -456,6 +462,31 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         const int quad_bar = 1 + quarter;  // named barrier of the kParts warps of this row quarter
         const float sl2 = A.sl2;
         uint32_t g = 0;
+        // epilogue of an item, deferred until the next item's first P is handed to the MMA so
+        // its O buffer is complete by then and the stores overlap the next item's tensor work
+        int pend_it = -1;
+        float pend_inv = 0.f;
+        uint16_t* pend_row = nullptr;
+        auto epilogue = [&]() {
+            const int buf = pend_it & 1;
+            mbar_wait(smem_u32(&o_full[buf]), (pend_it >> 1) & 1);
+            fence_after();
+#pragma unroll 1
+            for (int c = 0; c < kC / 32; ++c) {
+                float v[32];
+                ld32(tmem + lane_base + 256 + buf * 128 + part * kC + c * 32, v);
+                uint4* op = reinterpret_cast<uint4*>(pend_row + c * 32);
+                const float inv = pend_inv;
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8)
+                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
+                                        pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&o_free[buf]));
+            pend_it = -1;
+        };
         for (int it = 0; it < n_items; ++it) {
             int qt, head, b;
             items.get(it, qt, head, b);
@@ -517,7 +548,7 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
 #pragma unroll 1
                     for (int c = 0; c < kC / 32; ++c) {
                         float o[32];
-                        const uint32_t ta = tmem + lane_base + 256 + part * kC + c * 32;
+                        const uint32_t ta = tmem + lane_base + 256 + (it & 1) * 128 + part * kC + c * 32;
                         ld32(ta, o);
 #pragma unroll
                         for (int i = 0; i < 32; ++i) o[i] *= alpha;
@@ -532,6 +563,7 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(p_full));
+                if (pend_it >= 0) epilogue();  // previous item: its last P V was issued before this P
             }
             xsum[part * 128 + r] = l;
             asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");
@@ -541,21 +573,11 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");  // xsum reused next item
             const float inv = 1.f / lt;
             if (part == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
-            mbar_wait(smem_u32(o_full), it & 1);
-            fence_after();
-            uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + part * kC;
-#pragma unroll 1
-            for (int c = 0; c < kC / 32; ++c) {
-                float v[32];
-                ld32(tmem + lane_base + 256 + part * kC + c * 32, v);
-                uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8)
-                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
-                                        pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
-            }
-            fence_before();  // O reads complete before this warp's next P arrival lets P V overwrite O
+            pend_it = it;
+            pend_inv = inv;
+            pend_row = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + part * kC;
         }
+        if (pend_it >= 0) epilogue();
     }
     fence_before();
     __syncthreads();
@@ -1470,14 +1492,14 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     const int items = (s / kT) * nh * B;
     const int grid = items < kNumSMs ? items : kNumSMs;
     if (parts == 2) {
-        const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8;
+        const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
         static bool cfg2 = false;
         cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
         if (e != cudaSuccess) return e;
         flash_fwd_pk_kernel<2><<<grid, (4 + 8) * 32, smem, st>>>(mq, mk, mv, a);
         return launched(1);
     }
-    const size_t smem = 1024 + 6 * (size_t)kTile + 22 * 8;
+    const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
     static bool cfg4 = false;
     cudaError_t e = set_smem(flash_fwd_pk_kernel<4>, smem, cfg4);
     if (e != cudaSuccess) return e;
