@@ -31,6 +31,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the host AdamW team must not spin between CpuOptim ops on cores the lane threads need
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 CONFIGS = {
     "1.3b": dict(num_blocks=24, hidden=2048, heads=16, seq_len=1024, batch=8, vocab=50257),
@@ -263,11 +265,11 @@ def main():
     ap.add_argument("--cpu-mem-gib", type=int, default=0, help="default: 80%% of this host's DRAM")
     ap.add_argument("--e2e-steps", type=int, default=0, help="default: = --steps")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    # CPU Adam team
-    # (one core left for the lane threads; split between the ranks of a node under DP so N ranks
-    # do not oversubscribe the host — the host AdamW is DRAM-bound, profiles/r1/cpu_adam_scaling.txt)
+    # CPU Adam team: leave cores for the four lane threads, the clock sampler and Python (with
+    # every core in the team the compute lane thread was intermittently descheduled and the GPU
+    # idled); split between the ranks of a node under DP so N ranks do not oversubscribe the host
     ap.add_argument("--cpu-threads", type=int,
-                    default=max(1, ((os.cpu_count() or 8) - 1) // max(1, int(os.environ.get("WORLD_SIZE", "1")))))
+                    default=max(1, ((os.cpu_count() or 8) - 4) // max(1, int(os.environ.get("WORLD_SIZE", "1")))))
     ap.add_argument("--strategy", default="", help="force c,p,o (default: planner)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)

@@ -128,6 +128,7 @@ private:
 
     void plan(const ah_trainer_config& cfg);
     void allocate_and_init();
+    void reserve_pool();
     void build_iteration(Iter& it);
     void lane_main(int lane);
     void wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side = false);

@@ -27,16 +27,23 @@ K = int(sys.argv[1]) if len(sys.argv) > 1 else 10
 mode = sys.argv[2] if len(sys.argv) > 2 else "none"
 import contextlib  # noqa: E402
 from bench import ClockSampler  # noqa: E402
-for trial in range(8):
-    ctx = ClockSampler(0) if mode == "nvml" else contextlib.nullcontext()
+for trial in range(10):
+    ctx = ClockSampler(0) if mode in ("nvml", "all") else contextlib.nullcontext()
     if mode == "smi":
         ctx = ClockSampler(0)
         ctx._open_nvml = lambda: None
+    import ctypes as C
+    from paper_2503_01890_b200 import _native as N
+    if mode in ("gemm", "all"):
+        N.check(N.lib().ah_gemm_timing(1, None, None, None))
     with ctx:
         tr.timer(False)
         for i in range(K):
             tr.submit(tok[i % 4], tok[(i + 1) % 4])
         ms = tr.timer(True)
+    if mode in ("gemm", "all"):
+        g_ms, g_fl, g_n = C.c_double(), C.c_double(), C.c_int64()
+        N.check(N.lib().ah_gemm_timing(0, C.byref(g_ms), C.byref(g_fl), C.byref(g_n)))
     tr_ops = tr.trace()
     comp = sorted([o for o in tr_ops if o["tid"] == 1], key=lambda o: o["ts"])
     gaps = []
