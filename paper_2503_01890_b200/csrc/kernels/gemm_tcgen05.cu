@@ -71,6 +71,7 @@ struct Params {
     int vec16_c, vec16_aux;  // 16-byte rows (direct path)
     int staged;              // smem-transposed epilogue (fp32 outputs)
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
+    int wait_ns;              // AH_GEMM_WAIT_NS: suspend-time hint of the producer / epilogue waits (0)
     int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE (profiling only): 1 no epilogue, 2 no C store, 3 packs only
     int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
     int fast;                 // tma_c, alpha 1, beta 0, N % BN == 0, 16-byte operand rows: lean epilogue
@@ -103,6 +104,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
             " selp.u32 %0, 1, 0, p;\n}"
             : "=r"(done)
             : "r"(bar), "r"(parity)
+            : "memory");
+    }
+}
+// Pipeline waits of the producer / MMA / epilogue roles with a suspend-time hint: a role that
+// is ahead (the TMA producer, the epilogue during the main loop) is parked by the hardware
+// instead of re-issuing the probe — every probe is an issued warp instruction and power.
+__device__ __forceinline__ void mbar_wait_hint(uint32_t bar, uint32_t parity, uint32_t ns) {
+    if (ns == 0) return mbar_wait(bar, parity);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+            " selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity), "r"(ns)
             : "memory");
     }
 }
@@ -401,7 +417,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
-                    mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+                    mbar_wait_hint(smem_u32(&empty[stage]), phase ^ 1, (uint32_t)P.wait_ns);
                     const uint32_t a_dst = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_dst = smem_u32(sB + stage * B_BYTES);
                     const int k0 = kb * BK;
@@ -470,7 +486,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int si = 0; si < nseg; ++si) {
                 const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
-                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
+                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);  // MMA waits: latency-critical, no hint
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
@@ -526,7 +542,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         for (int si = 0; si < nseg; ++si) {
             const Tile T = segment<CS>(P, si, BN, crank);
             if (T.skip) continue;
-            mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+            mbar_wait_hint(smem_u32(&tfull[acc]), acc_phase, (uint32_t)P.wait_ns);
             tc_fence_after();
             if (T.role == 2) {  // stream-K suffix: wait for the previous CTA's partial of this tile
                 if (warp == 0 && lane == 0) {
@@ -1104,6 +1120,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
             return e ? std::atoi(e) : 0;
         }();
         P.dbg_no_store = no_store;
+        static const int wait_ns = [] {
+            const char* e = std::getenv("AH_GEMM_WAIT_NS");
+            return e ? std::atoi(e) : 0;
+        }();
+        P.wait_ns = wait_ns;
         P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
         P.vec16_res = (reinterpret_cast<uintptr_t>(g.residual) % 16 == 0) && g.ld_res % 8 == 0 && g.res_s1 % 8 == 0 &&
                       g.res_s2 % 8 == 0;
