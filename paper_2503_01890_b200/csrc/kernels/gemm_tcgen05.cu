@@ -72,6 +72,7 @@ struct Params {
     int staged;              // smem-transposed epilogue (fp32 outputs)
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
     int wait_ns;              // AH_GEMM_WAIT_NS: suspend-time hint of the producer / epilogue waits (0)
+    int mma_wait_ns;          // AH_GEMM_MMA_WAIT_NS: same for the MMA issuer's waits (0)
     int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE (profiling only): 1 no epilogue, 2 no C store, 3 packs only
     int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
     int fast;                 // tma_c, alpha 1, beta 0, N % BN == 0, 16-byte operand rows: lean epilogue
@@ -486,11 +487,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int si = 0; si < nseg; ++si) {
                 const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
-                mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);  // MMA waits: latency-critical, no hint
+                mbar_wait_hint(smem_u32(&tempty[acc]), acc_phase ^ 1, (uint32_t)P.mma_wait_ns);  // latency-critical
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
-                    mbar_wait(smem_u32(&full[stage]), phase);
+                    mbar_wait_hint(smem_u32(&full[stage]), phase, (uint32_t)P.mma_wait_ns);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
@@ -1125,6 +1126,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
             return e ? std::atoi(e) : 0;
         }();
         P.wait_ns = wait_ns;
+        static const int mma_wait_ns = [] {
+            const char* e = std::getenv("AH_GEMM_MMA_WAIT_NS");
+            return e ? std::atoi(e) : 0;
+        }();
+        P.mma_wait_ns = mma_wait_ns;
         P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
         P.vec16_res = (reinterpret_cast<uintptr_t>(g.residual) % 16 == 0) && g.ld_res % 8 == 0 && g.res_s1 % 8 == 0 &&
                       g.res_s2 % 8 == 0;
