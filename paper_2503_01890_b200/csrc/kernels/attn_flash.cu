@@ -331,11 +331,14 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint64_t* v_empty = bar + 10;  // [2]
     uint64_t* s_full = bar + 12;   // [2]
     uint64_t* s_free = bar + 14;   // [2]
+    // [2] P_g stored (indexed by g & 1): a softmax warp that skips the rescale wait can reach
+    // tile g + 1 (its S is issued before P V_g) and arrive while slower warps are still on tile g,
+    // so one barrier would complete the phase of tile g without them
     uint64_t* p_full = bar + 16;
-    uint64_t* pv_done = bar + 17;
     uint64_t* o_full = bar + 18;  // [2] O buffer of an item complete
     uint64_t* o_free = bar + 20;  // [2] softmax warps have drained an O buffer
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 22);
+    uint64_t* pv_done = bar + 22;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 23);
     constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
     constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
     // statically shared (not carved from the aligned dynamic block) so the compiler emits LDS/STS
@@ -359,9 +362,9 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             mbar_init(smem_u32(&s_full[i]), 1);
             mbar_init(smem_u32(&s_free[i]), kSoft);
         }
-        mbar_init(smem_u32(p_full), kSoft);
         mbar_init(smem_u32(pv_done), 1);
         for (int i = 0; i < 2; ++i) {
+            mbar_init(smem_u32(&p_full[i]), kSoft);
             mbar_init(smem_u32(&o_full[i]), 1);
             mbar_init(smem_u32(&o_free[i]), kSoft);
         }
@@ -442,7 +445,7 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                     if (s_it < n_items) issue_next_S();  // scores of the next tile overlap softmax of this one
                     const int st = g & 1;
                     if (j == 0 && it >= 2) mbar_wait(smem_u32(&o_free[it & 1]), ((it >> 1) & 1) ^ 1);
-                    mbar_wait(smem_u32(p_full), g & 1);
+                    mbar_wait(smem_u32(&p_full[st]), (g >> 1) & 1);
                     mbar_wait(smem_u32(&v_full[st]), (g >> 1) & 1);
                     fence_after();
                     const uint32_t va = smem_u32(sV + st * kTile);
@@ -562,7 +565,7 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                     st16(tmem + lane_base + st * 128 + part * (kC / 2), *reinterpret_cast<float(*)[16]>(w));
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(p_full));
+                if (lane == 0) mbar_arrive(smem_u32(&p_full[st]));
                 if (pend_it >= 0) epilogue();  // previous item: its last P V was issued before this P
             }
             xsum[part * 128 + r] = l;

@@ -76,7 +76,9 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     d_.s = cfg.seq_len;
     d_.B = cfg.batch;
     d_.V = cfg.vocab;
-    d_.Vp = (int)round_up((size_t)cfg.vocab, 128);
+    // padded vocabulary: a multiple of the 256-column GEMM tile, so the LM-head GEMMs take the
+    // lean epilogue (N % 256 == 0); padding rows of wte are zero and masked out of the loss
+    d_.Vp = (int)round_up((size_t)cfg.vocab, 256);
     if (d_.L < 1 || d_.h % 64 || d_.nh < 1 || d_.h % d_.nh || d_.hd % 64 || d_.s % 128 || d_.B < 1 || d_.V < 2 ||
         d_.T() > 16384)
         throw std::invalid_argument(
@@ -1012,7 +1014,7 @@ ah_hw_profile profile_block(const ah_trainer_config& cfg) {
     d.s = cfg.seq_len;
     d.B = cfg.batch;
     d.V = cfg.vocab;
-    d.Vp = (int)round_up((size_t)cfg.vocab, 128);
+    d.Vp = (int)round_up((size_t)cfg.vocab, 256);
     const size_t mp = d.m_p(), T = d.T(), h = d.h;
     auto ok = [](cudaError_t e, const char* w) {
         if (e != cudaSuccess) throw std::runtime_error(std::string(w) + ": " + cudaGetErrorString(e));

@@ -17,6 +17,9 @@ def _ptr(t):
 def layernorm_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor):
     """x [rows, h] bf16 CUDA -> (y bf16, mean fp32 [rows], rstd fp32 [rows])."""
     rows, h = x.shape
+    for t in (x, gamma, beta):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("layernorm_fwd: x, gamma, beta must be contiguous bf16 CUDA tensors")
     y = torch.empty_like(x)
     mean = torch.empty(rows, dtype=torch.float32, device=x.device)
     rstd = torch.empty(rows, dtype=torch.float32, device=x.device)
@@ -31,6 +34,11 @@ def layernorm_fwd(x: torch.Tensor, gamma: torch.Tensor, beta: torch.Tensor):
 def layernorm_bwd(dy, x, mean, rstd, gamma, dres=None, bias_sums=False):
     """-> (dx [rows, h], dgamma_dbeta [2h], dres_colsum [h] | None, dx_colsum [h] | None), bf16."""
     rows, h = x.shape
+    for t in (dy, x, gamma) + (() if dres is None else (dres,)):
+        if t.dtype != torch.bfloat16 or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("layernorm_bwd: dy, x, gamma, dres must be contiguous bf16 CUDA tensors")
+    if mean.dtype != torch.float32 or rstd.dtype != torch.float32:
+        raise ValueError("layernorm_bwd: mean / rstd must be fp32")
     dx = torch.empty_like(x)
     dgdb = torch.empty(2 * h, dtype=torch.bfloat16, device=x.device)
     cr = torch.empty(h, dtype=torch.bfloat16, device=x.device) if bias_sums and dres is not None else None
