@@ -28,7 +28,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <string>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -997,6 +1000,7 @@ struct TimingState {
     struct Rec {
         cudaEvent_t a, b;
         double flops;
+        std::string shape;  // for the per-shape dump (AH_GEMM_TIMING_DUMP)
     };
     std::vector<Rec> recs;
     std::vector<cudaEvent_t> pool;  // pre-created timing events: no cudaEventCreate on the launch path
@@ -1030,6 +1034,7 @@ void timing_collect(double* total_ms, double* total_flops, long long* launches) 
     std::lock_guard<std::mutex> lk(timing().mu);
     double ms = 0.0, fl = 0.0;
     long long n = 0;
+    std::map<std::string, std::tuple<long long, double, double>> by_shape;
     for (auto& r : timing().recs) {
         float t = 0.f;
         cudaEventSynchronize(r.b);
@@ -1037,11 +1042,23 @@ void timing_collect(double* total_ms, double* total_flops, long long* launches) 
             ms += t;
             fl += r.flops;
             ++n;
+            auto& a = by_shape[r.shape];
+            std::get<0>(a) += 1;
+            std::get<1>(a) += t;
+            std::get<2>(a) += r.flops;
         }
         timing().pool.push_back(r.a);
         timing().pool.push_back(r.b);
     }
     timing().recs.clear();
+    if (const char* path = std::getenv("AH_GEMM_TIMING_DUMP"); path && n > 0) {
+        if (FILE* f = std::fopen(path, "a")) {  // one line per shape: launches, ms, TFLOP/s
+            for (auto& [k, a] : by_shape)
+                std::fprintf(f, "%s n=%lld ms=%.3f tflops=%.1f\n", k.c_str(), std::get<0>(a), std::get<1>(a),
+                             std::get<2>(a) / (std::get<1>(a) * 1e-3) / 1e12);
+            std::fclose(f);
+        }
+    }
     if (total_ms) *total_ms = ms;
     if (total_flops) *total_flops = fl;
     if (launches) *launches = n;
@@ -1160,21 +1177,30 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
                 2 * tail <= G && P.k_blocks >= 64) ? 1 : 0;  // measured: +4% at K=8192, -2% at K=2048
     }
     if (P.sk) {
+        // partial-tile workspace + hand-off flags, one set per (device, stream): GEMMs on
+        // different streams (e.g. in-process DP ranks) may run concurrently; on one stream they
+        // are ordered, so the epoch counter tells consecutive launches apart
+        struct SkState {
+            float* ws = nullptr;
+            unsigned* flags = nullptr;
+            unsigned epoch = 0;
+        };
         static std::mutex mu;
-        static float* ws = nullptr;
-        static unsigned* flags = nullptr;
-        static unsigned epoch = 0;
+        static std::map<std::pair<int, cudaStream_t>, SkState> states;
+        int dev = 0;
+        cudaGetDevice(&dev);
         std::lock_guard<std::mutex> lk(mu);
-        if (!ws) {
-            if (cudaMalloc(&ws, (size_t)kNumSMs * BM * 256 * 4) != cudaSuccess ||
-                cudaMalloc(&flags, kNumSMs * sizeof(unsigned)) != cudaSuccess ||
-                cudaMemset(flags, 0, kNumSMs * sizeof(unsigned)) != cudaSuccess)
+        SkState& S = states[{dev, stream}];
+        if (!S.ws) {
+            if (cudaMalloc(&S.ws, (size_t)kNumSMs * BM * 256 * 4) != cudaSuccess ||
+                cudaMalloc(&S.flags, kNumSMs * sizeof(unsigned)) != cudaSuccess ||
+                cudaMemsetAsync(S.flags, 0, kNumSMs * sizeof(unsigned), stream) != cudaSuccess)
                 return cudaErrorMemoryAllocation;
         }
-        P.sk_ws = ws;
-        P.sk_flags = flags;
-        P.sk_epoch = ++epoch;
-        if (P.sk_epoch == 0) P.sk_epoch = ++epoch;  // flags start at 0
+        P.sk_ws = S.ws;
+        P.sk_flags = S.flags;
+        P.sk_epoch = ++S.epoch;
+        if (P.sk_epoch == 0) P.sk_epoch = ++S.epoch;  // flags start at 0
     }
     CUtensorMap ma, mb;
     const bool ok_a = g.a_mn_major
@@ -1219,7 +1245,11 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     if (timed) {
         cudaEventRecord(tb, stream);
         std::lock_guard<std::mutex> lk(timing().mu);
-        timing().recs.push_back({ta, tb, executed_flops(g)});
+        char shape[160];
+        std::snprintf(shape, sizeof shape, "M=%d N=%d K=%d z=%d a_mn=%d b_mn=%d causal=%d epi=%d f32=%d BN=%d CS=%d sk=%d grid=%d",
+                      g.M, g.N, g.K, g.batch1 * (g.batch2 > 0 ? g.batch2 : 1), g.a_mn_major, g.b_mn_major, g.causal,
+                      g.epilogue, g.c_f32, BN, CS, (int)P.sk, grid);
+        timing().recs.push_back({ta, tb, executed_flops(g), shape});
     }
     return e;
 }

@@ -164,3 +164,26 @@ def test_gemm_stream_k_shapes(cuda_device, native, M, N, K, a_mn, b_mn):
     torch.cuda.synchronize()
     ref = A.float() @ B.float().T + bias.float() + res.float()
     assert rel_err(C, ref) < 1e-2
+
+
+def test_gemm_stream_k_concurrent_streams(cuda_device, native):
+    """Stream-K launches on different streams (in-process DP ranks) may overlap: each stream
+    has its own partial-tile workspace and flags, so concurrent results equal serial ones."""
+    from paper_2503_01890_b200.gemm import gemm
+    M, N, K = 8192, 2048, 8192
+    ops = [operands(M, N, K, 0, 0, seed=11 + i) for i in range(2)]
+    serial = []
+    for A, B, a_arg, b_arg in ops:
+        C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+        gemm(a_arg, b_arg, C)
+        serial.append(C)
+    torch.cuda.synchronize()
+    streams = [torch.cuda.Stream() for _ in ops]
+    outs = [torch.empty(M, N, device="cuda", dtype=torch.bfloat16) for _ in ops]
+    for _ in range(20):
+        for (A, B, a_arg, b_arg), st, C in zip(ops, streams, outs):
+            with torch.cuda.stream(st):
+                gemm(a_arg, b_arg, C, stream=st)
+    torch.cuda.synchronize()
+    for C, ref in zip(outs, serial):
+        assert torch.equal(C, ref)
