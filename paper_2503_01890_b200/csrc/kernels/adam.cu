@@ -169,6 +169,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 adam_tma_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
                 const uint16_t* __restrict__ g, uint16_t* __restrict__ pout, size_t n_main,
                 AdamScalars k, const int* __restrict__ skip, float* __restrict__ stats) {
+    pdl_launch_dependents();
+    pdl_wait();
     if (skip != nullptr && *skip != 0) return;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -301,6 +303,8 @@ __global__ void adam_scalar_kernel(float* p, float* m, float* v, const uint16_t*
 
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst,
                                      size_t n_vec) {
+    pdl_launch_dependents();
+    pdl_wait();
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_vec; j += stride) {
         const float4 a = ld_f4(src + j * 8);
@@ -383,13 +387,13 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
             (void)attr;
             const size_t nm = n_vec * 8;
             if (a.p_bf16 && a.stats)
-                adam_tma_kernel<true, true><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+                launch_ex((adam_tma_kernel<true, true>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
             else if (a.p_bf16)
-                adam_tma_kernel<true, false><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+                launch_ex((adam_tma_kernel<true, false>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
             else if (a.stats)
-                adam_tma_kernel<false, true><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+                launch_ex((adam_tma_kernel<false, true>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
             else
-                adam_tma_kernel<false, false><<<grid, kTmaThreads, kTmaSmem, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
+                launch_ex((adam_tma_kernel<false, false>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
         } else if (n_vec) {
             int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
             if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
@@ -417,7 +421,7 @@ cudaError_t launch_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, cuda
     size_t done = 0;
     if (aligned16(src) && aligned16(dst)) {
         const size_t n_vec = n / 8;
-        if (n_vec) cast_f32_bf16_kernel<<<grid_for(n_vec, 256, 8), 256, 0, stream>>>(src, dst, n_vec);
+        if (n_vec) launch_ex(cast_f32_bf16_kernel, dim3(grid_for(n_vec, 256, 8)), dim3(256), 0, stream, 1, src, dst, n_vec);
         done = n_vec * 8;
     }
     if (done < n) cast_tail_kernel<<<1, 256, 0, stream>>>(src, dst, done, n);

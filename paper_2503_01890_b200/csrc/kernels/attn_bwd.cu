@@ -233,6 +233,8 @@ attn_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__
 // (b, q, head) row: 16 lanes x 16-byte loads cover the 128 head columns; grid-stride.
 __global__ void attn_bwd_dot_kernel(const uint16_t* __restrict__ dO, const uint16_t* __restrict__ O, float* __restrict__ D,
                                     int B, int s, int nh) {
+    pdl_launch_dependents();
+    pdl_wait();
     const long long rows = (long long)B * s * nh;
     const int sub = threadIdx.x & 15;
     for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; w < rows;
@@ -291,7 +293,7 @@ bool map4(CUtensorMap* m, const void* base, cuuint64_t d0, cuuint64_t d1, cuuint
 bool attn_bwd_supported(int hd, int s) { return hd == kHD && s % kT == 0; }
 
 cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st) {
-    attn_bwd_dot_kernel<<<kNumSMs * 8, 256, 0, st>>>(dO, O, D, B, s, nh);
+    launch_ex(attn_bwd_dot_kernel, dim3(kNumSMs * 8), dim3(256), 0, st, 1, dO, O, D, B, s, nh);
     return launched(1);
 }
 
@@ -299,7 +301,7 @@ cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO,
                      uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st) {
     if (!attn_bwd_supported(hd, s)) return cudaErrorInvalidValue;
     const int h = nh * hd;
-    attn_bwd_dot_kernel<<<kNumSMs * 8, 256, 0, st>>>(dO, O, D, B, s, nh);
+    launch_ex(attn_bwd_dot_kernel, dim3(kNumSMs * 8), dim3(256), 0, st, 1, dO, O, D, B, s, nh);
     launched(1);
     CUtensorMap mq, mv, mdo, mp;
     const cuuint64_t row3 = 3ull * h;

@@ -380,6 +380,8 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_holder;  // S/P[0] 0-127, S/P[1] 128-255, O[0] 256-383, O[1] 384-511
+    pdl_launch_dependents();  // setup above overlapped the previous kernel (PDL); data from here on
+    pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer =====
@@ -1187,6 +1189,8 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     __syncthreads();
     fence_after();
     const uint32_t tmem = *tmem_holder;
+    pdl_launch_dependents();  // setup above overlapped the previous kernel (PDL); data from here on
+    pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {  // ===== TMA producer: K, V per item; Q, dO per query tile =====
@@ -1499,7 +1503,7 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
         static bool cfg2 = false;
         cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
         if (e != cudaSuccess) return e;
-        flash_fwd_pk_kernel<2><<<grid, (4 + 8) * 32, smem, st>>>(mq, mk, mv, a);
+        launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, a);
         return launched(1);
     }
     const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
@@ -1539,7 +1543,7 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
         e = set_smem(flash_bwd_t_kernel, smem, cfg3);
         if (e != cudaSuccess) return e;
         const int items = (s / kT) * nh * B;
-        flash_bwd_t_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, mdo, a);
+        launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, a);
         return launched(1);
     }
     if (variant == 0) {

@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(256) softmax_bwd_reg_kernel(const uint16_t* __
 // out[n] = sum_{r ascending} part[r][n]; 8 row groups x 32 columns per CTA, fixed order.
 __global__ void __launch_bounds__(256) colsum_finish_wide_kernel(const float* __restrict__ part, int R, int N,
                                                                void* out, int out_f32) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float red[8][33];
     const int c = threadIdx.x & 31, g = threadIdx.x >> 5;
     const int n = blockIdx.x * 32 + c;
@@ -152,7 +154,7 @@ cudaError_t softmax_bwd2(const uint16_t* P, const float* dP, uint16_t* dS, long 
 }
 
 cudaError_t colsum_finish_wide(const float* part, int R, int N, void* out, int out_f32, cudaStream_t st) {
-    colsum_finish_wide_kernel<<<(N + 31) / 32, 256, 0, st>>>(part, R, N, out, out_f32);
+    launch_ex(colsum_finish_wide_kernel, dim3((N + 31) / 32), dim3(256), 0, st, 1, part, R, N, out, out_f32);
     return launched(1);
 }
 

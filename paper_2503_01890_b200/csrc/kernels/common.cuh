@@ -61,6 +61,11 @@ __device__ __forceinline__ void st_u4(void* p, uint4 v) {
                  : "memory");
 }
 
+// Programmatic dependent launch: block until the previous grid on the stream has completed and
+// its writes are visible (no-op when launched without the attribute); let the next grid launch.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

@@ -410,6 +410,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // setup above overlapped the previous kernel's tail (PDL); operands / outputs only from here
+    pdl_launch_dependents();
+    pdl_wait();
 
     if (warp == kWarpTMA) {
         if (lane == 0) {
@@ -973,23 +976,7 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, const 
         if (e != cudaSuccess) return e;
         configured = true;
     }
-    if (CS == 1) {
-        gemm_kernel<BN, STAGES, CS><<<grid, kThreads, sm, stream>>>(a, b, c, P);
-        return launched(1);
-    }
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_kernel<BN, STAGES, CS>, a, b, c, P);
+    const cudaError_t e = launch_ex(gemm_kernel<BN, STAGES, CS>, dim3(grid), dim3(kThreads), sm, stream, CS, a, b, c, P);
     launched(1);
     return e != cudaSuccess ? e : cudaGetLastError();
 }

@@ -172,6 +172,8 @@ __global__ void colsum_partial_kernel(const uint16_t* __restrict__ X, int T, int
 // row lanes are combined in smem in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) colsum_partial2_kernel(const uint16_t* __restrict__ X, int T, int N, int ldx,
                                                               int rows, float* __restrict__ part) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float red[8][256];
     const int cg = threadIdx.x & 31, ry = threadIdx.x >> 5;
     const int c = (blockIdx.x * 32 + cg) * 8;
@@ -332,6 +334,8 @@ __device__ __forceinline__ uint32_t bf16x2_max(uint32_t a, uint32_t b) {
 }
 __global__ void __launch_bounds__(kCeThreads, 1)
 ce_reg_kernel(uint16_t* logits, const int* __restrict__ tgt, float* __restrict__ loss, int V, int ld, float dscale) {
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ float red_m[32], red_s[32];
     constexpr uint32_t kNegInf2 = 0xff80ff80u;  // two bf16 -inf: padding / out-of-row lanes
     const int row = blockIdx.x;
@@ -524,7 +528,7 @@ cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* 
     const int R = colsum_rows(T);
     const int rows = (T + R - 1) / R;
     if (N % 8 == 0 && ldx % 8 == 0 && reinterpret_cast<uintptr_t>(X) % 16 == 0)
-        colsum_partial2_kernel<<<dim3((N + 255) / 256, R), 256, 0, st>>>(X, T, N, ldx, rows, part);
+        launch_ex(colsum_partial2_kernel, dim3(dim3((N + 255) / 256, R)), dim3(256), 0, st, 1, X, T, N, ldx, rows, part);
     else
         colsum_partial_kernel<<<dim3((N / 8 + 127) / 128, R), 128, 0, st>>>(X, T, N, ldx, rows, part);
     launched(1);
@@ -550,7 +554,7 @@ cudaError_t gelu_bwd(const uint16_t* dgelu, const uint16_t* pre, uint16_t* dpre,
 cudaError_t cross_entropy(uint16_t* logits, const int* tgt, float* loss, int T, int V, int ld, float dscale,
                           cudaStream_t st) {
     if (ld % 8 == 0 && ld <= kCeThreads * 8 * kCeVec && reinterpret_cast<uintptr_t>(logits) % 16 == 0)
-        ce_reg_kernel<<<T, kCeThreads, 0, st>>>(logits, tgt, loss, V, ld, dscale);
+        launch_ex(ce_reg_kernel, dim3(T), dim3(kCeThreads), 0, st, 1, logits, tgt, loss, V, ld, dscale);
     else
         ce_kernel<<<T, 512, 0, st>>>(logits, tgt, loss, V, ld, dscale);
     return launched(1);

@@ -33,6 +33,7 @@ cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, floa
 }  // namespace ah
 
 #include <atomic>
+#include <utility>
 namespace ah {
 // Number of kernels this library has launched (for the bench's gpu_launches claim).
 inline std::atomic<long long>& kernel_launch_counter() {
@@ -43,4 +44,39 @@ inline cudaError_t launched(int n) {
     kernel_launch_counter().fetch_add(n, std::memory_order_relaxed);
     return cudaGetLastError();
 }
+
+// Programmatic dependent launch (on unless AH_PDL=0): kernels whose every global-memory access
+// follows pdl_wait() (common.cuh) are launched with programmatic stream serialisation, so their
+// launch and prologue (barrier init, TMEM allocation, tensor-map prefetch) overlap the tail of
+// the previous kernel on the stream instead of following its completion.
+bool pdl_enabled();
+
+#ifdef __CUDACC__
+template <typename... KArgs, typename... Args>
+cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, int cluster,
+                      Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int n = 0;
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = cluster;
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    if (pdl_enabled()) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);  // callers count via launched()
+}
+#endif
 }  // namespace ah

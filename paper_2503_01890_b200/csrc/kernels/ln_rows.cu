@@ -142,6 +142,8 @@ __global__ void __launch_bounds__(768) ln_fwd_rows_kernel(const uint16_t* __rest
         bar_expect(&bars[st], rb);
         bulk_row(tc_smem(sm + st * plan.stage_bytes), x + (size_t)(r0 + j) * h, rb, tc_smem(&bars[st]));
     };
+    pdl_launch_dependents();
+    pdl_wait();
     if (threadIdx.x == 0) {
         for (int i = 0; i < ring; ++i) bar_init(&bars[i]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -219,6 +221,8 @@ __global__ void __launch_bounds__(256) ln_fwd_warp_kernel(const uint16_t* __rest
                                                          float* __restrict__ mean, float* __restrict__ rstd, int T) {
     constexpr int h = NC * 256;
     const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    pdl_launch_dependents();
+    pdl_wait();
     if (row >= T) return;
     const uint16_t* xr = x + (size_t)row * h + lane * 8;
     uint4 w[NC];
@@ -292,6 +296,8 @@ __global__ void __launch_bounds__(768) ln_bwd_rows_kernel(const uint16_t* __rest
         bulk_row(tc_smem(d + rb), dy + off, rb, tc_smem(&bars[st]));
         if (kRes) bulk_row(tc_smem(d + 2 * rb), dres + off, rb, tc_smem(&bars[st]));
     };
+    pdl_launch_dependents();
+    pdl_wait();
     if (threadIdx.x == 0) {
         for (int i = 0; i < ring; ++i) bar_init(&bars[i]);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -404,6 +410,8 @@ __global__ void __launch_bounds__(512) ln_finish_kernel(const float* __restrict_
                                                         SegOut out) {
     __shared__ float4 red[16][8];
     const int cg = threadIdx.x & 7, rl = threadIdx.x >> 3;  // rl: 0..63
+    pdl_launch_dependents();
+    pdl_wait();
     const int n = (blockIdx.x * 8 + cg) * 4;
     const int N = nseg * h;
     float4 acc[8];
@@ -473,7 +481,8 @@ int launch_bwd(cudaStream_t st, const uint16_t* dy, const uint16_t* x, const flo
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, RingPlan(h, nt, (T + kNumSMs - 1) / kNumSMs).total);
     const int cap = ln_bwd_ctas(T), ctas = std::min(cap, kNumSMs * std::max(1, occ));
     const int rows = (T + ctas - 1) / ctas, grid = (T + rows - 1) / rows;
-    kern<<<grid, threads, RingPlan(h, nt, rows).total, st>>>(dy, x, mean, rstd, g, dres, dx, part, T, h, rows);
+    launch_ex(kern, dim3(grid), dim3(threads), RingPlan(h, nt, rows).total, st, 1, dy, x, mean, rstd, g, dres, dx, part, T,
+              h, rows);
     return grid;
 }
 
@@ -487,10 +496,10 @@ cudaError_t ln_fwd_rows(const uint16_t* x, const uint16_t* g, const uint16_t* b,
                         float* rstd, int T, int h, cudaStream_t st) {
     if (T <= 0) return cudaSuccess;
     switch (h) {  // register-resident warp-per-row forms for the common widths
-        case 768: ln_fwd_warp_kernel<3><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
-        case 1024: ln_fwd_warp_kernel<4><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
-        case 2048: ln_fwd_warp_kernel<8><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
-        case 4096: ln_fwd_warp_kernel<16><<<(T + 7) / 8, 256, 0, st>>>(x, g, b, y, mean, rstd, T); return launched(1);
+        case 768: launch_ex(ln_fwd_warp_kernel<3>, dim3((T + 7) / 8), dim3(256), 0, st, 1, x, g, b, y, mean, rstd, T); return launched(1);
+        case 1024: launch_ex(ln_fwd_warp_kernel<4>, dim3((T + 7) / 8), dim3(256), 0, st, 1, x, g, b, y, mean, rstd, T); return launched(1);
+        case 2048: launch_ex(ln_fwd_warp_kernel<8>, dim3((T + 7) / 8), dim3(256), 0, st, 1, x, g, b, y, mean, rstd, T); return launched(1);
+        case 4096: launch_ex(ln_fwd_warp_kernel<16>, dim3((T + 7) / 8), dim3(256), 0, st, 1, x, g, b, y, mean, rstd, T); return launched(1);
         default: break;
     }
     const int threads = h / 8;
@@ -505,7 +514,8 @@ cudaError_t ln_fwd_rows(const uint16_t* x, const uint16_t* g, const uint16_t* b,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ln_fwd_rows_kernel, threads, plan.total);
     const int want = kNumSMs * std::max(1, occ);
     const int rows = (T + want - 1) / want;
-    ln_fwd_rows_kernel<<<(T + rows - 1) / rows, threads, plan.total, st>>>(x, g, b, y, mean, rstd, T, h, rows);
+    launch_ex(ln_fwd_rows_kernel, dim3((T + rows - 1) / rows), dim3(threads), plan.total, st, 1, x, g, b, y, mean, rstd, T, h,
+              rows);
     return launched(1);
 }
 
@@ -534,14 +544,15 @@ cudaError_t ln_bwd_rows(const uint16_t* dy, const uint16_t* x, const float* mean
     if (cr) out.p[nseg++] = dres_colsum;
     if (cx) {
         if (!cr) {  // keep segment index == part column block: finish segment 3 separately
-            ln_finish_kernel<<<(2 * h + 31) / 32, 512, 0, st>>>(part, grid, 4 * h, h, 2, out);
+            launch_ex(ln_finish_kernel, dim3((2 * h + 31) / 32), dim3(512), 0, st, 1, part, grid, 4 * h, h, 2, out);
             SegOut o2{{dx_colsum, nullptr, nullptr, nullptr}};
-            ln_finish_kernel<<<(h + 31) / 32, 512, 0, st>>>(part + 3 * h, grid, 4 * h, h, 1, o2);
+            launch_ex(ln_finish_kernel, dim3((h + 31) / 32), dim3(512), 0, st, 1, (const float*)(part + 3 * h), grid, 4 * h, h, 1,
+                      o2);
             return launched(3);
         }
         out.p[nseg++] = dx_colsum;
     }
-    ln_finish_kernel<<<(nseg * h + 31) / 32, 512, 0, st>>>(part, grid, 4 * h, h, nseg, out);
+    launch_ex(ln_finish_kernel, dim3((nseg * h + 31) / 32), dim3(512), 0, st, 1, part, grid, 4 * h, h, nseg, out);
     return launched(2);
 }
 

@@ -144,3 +144,29 @@ def test_checkpoint_resume_across_plans(cuda_device, native, tmp_path):
     assert loss == ref_loss[-1]
     for a, b in zip(state, ref_state):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_long_run_is_deterministic_and_finite(cuda_device, native):
+    """Two fresh trainers, offload + recompute plan, 60 pipelined steps memorising 4 batches at
+    a high learning rate (attention sharpens, so the flash forward's lazy rescales fire): the loss
+    sequences must be bit-identical and finite. Timing-dependent races show up here as a
+    divergence part-way through (how the flash P-ready race was found)."""
+    from paper_2503_01890_b200.trainer import AdamConfig, ModelConfig, PlanConfig, Trainer
+    model = dict(num_blocks=4, hidden=512, heads=4, seq_len=512, batch=4, vocab=4096)
+    rng = np.random.default_rng(3)
+    data = [(rng.integers(0, 4096, size=(4, 512), dtype=np.int32), rng.integers(0, 4096, size=(4, 512), dtype=np.int32))
+            for _ in range(4)]
+    runs = []
+    for _ in range(2):
+        tr = Trainer(ModelConfig(**model), PlanConfig(c_hat=2, p_hat=2, o_hat=2, fine_tune=False, gpu_mem_budget=1 << 40),
+                     AdamConfig(lr=2e-3), seed=5, cpu_threads=4)
+        losses = []
+        for k in range(60):
+            tr.submit(*data[k % 4])
+            if k % 4 == 3:
+                losses.append(tr.drain())
+        tr.close()
+        runs.append(losses)
+    assert all(np.isfinite(runs[0])), runs[0]
+    assert runs[0] == runs[1]
+    assert runs[0][-1] < runs[0][0] - 0.5  # it learns
