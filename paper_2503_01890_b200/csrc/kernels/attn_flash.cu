@@ -1132,9 +1132,14 @@ __device__ __forceinline__ uint32_t tsA(uint32_t base, int t) { return base + (t
 __global__ void __launch_bounds__(kThreads, 1)
 flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                   const BwdParams A) {
+                   const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
+    // dS^T leaves through per-warp 32 x 64 smem slabs and TMA bulk stores when the dynamic smem
+    // base is 1024-aligned (the request has no alignment slack left for the slabs); otherwise
+    // each thread stores its 128-byte row directly
+    const bool tma_ds = sm == smem_raw;
+    uint8_t* slabs = sm + 6 * kTile + 3072;  // [8 softmax warps][32 rows x 128 B], SWIZZLE_128B images
     uint8_t* sK = sm;
     uint8_t* sV = sm + kTile;
     uint8_t* sQ = sm + 2 * kTile;   // [2]
@@ -1361,9 +1366,29 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(smem_u32(ds_full));
-                uint4* dst = reinterpret_cast<uint4*>(dsrow + (size_t)qi * kT);  // dS^T row -> HBM (dQ GEMM)
+                if (tma_ds) {  // dS^T slab -> HBM (dQ GEMM): one bulk tensor store per warp and tile
+                    uint8_t* slab = slabs + (warp - 4) * 4096;
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slab free
+                    __syncwarp();
 #pragma unroll
-                for (int k8 = 0; k8 < 8; ++k8) dst[k8] = make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+                    for (int k8 = 0; k8 < 8; ++k8)
+                        *reinterpret_cast<uint4*>(slab + lane * 128 + ((k8 ^ (lane & 7)) << 4)) =
+                            make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        asm volatile(
+                            "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tmdS)),
+                            "r"(smem_u32(slab)), "r"(qi * kT + half * 64), "r"(kt * kT + quarter * 32), "r"(head), "r"(b)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else {
+                    uint4* dst = reinterpret_cast<uint4*>(dsrow + (size_t)qi * kT);  // dS^T row -> HBM (dQ GEMM)
+#pragma unroll
+                    for (int k8 = 0; k8 < 8; ++k8) dst[k8] = make_uint4(o[4 * k8], o[4 * k8 + 1], o[4 * k8 + 2], o[4 * k8 + 3]);
+                }
             }
             mbar_wait(smem_u32(acc_full), it & 1);
             fence_after();
@@ -1387,6 +1412,7 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(acc_free));
         }
+        if (tma_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dS^T written
     }
     fence_before();
     __syncthreads();
@@ -1538,12 +1564,14 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     a.dqkv = dqkv;
     const int variant = flash_bwd_variant();
     if (variant == 2) {  // transposed persistent kernel: dS^T [B][nh][key][query]
-        const size_t smem = 1024 + 6 * (size_t)kTile + 2048 + 16 * 8;
+        // tiles | lse/D stages (2 KB) | barriers (<= 1 KB) | 8 dS^T slabs (32 KB): the 227 KB maximum
+        const size_t smem = 6 * (size_t)kTile + 3072 + 8 * 4096;
         static bool cfg3 = false;
         e = set_smem(flash_bwd_t_kernel, smem, cfg3);
         if (e != cudaSuccess) return e;
         const int items = (s / kT) * nh * B;
-        launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, a);
+        launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, mds,
+                  a);
         return launched(1);
     }
     if (variant == 0) {
