@@ -1132,10 +1132,11 @@ __device__ __forceinline__ uint32_t tsA(uint32_t base, int t) { return base + (t
 __global__ void __launch_bounds__(kThreads, 1)
 flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                   const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
+                   const __grid_constant__ CUtensorMap tmdS, const __grid_constant__ CUtensorMap tmdQKV,
+                   const BwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
-    // dS^T leaves through per-warp 32 x 64 smem slabs and TMA bulk stores when the dynamic smem
+    // dS^T (and the dV / dK epilogue) leaves through per-warp 32 x 64 smem slabs and TMA bulk stores when the dynamic smem
     // base is 1024-aligned (the request has no alignment slack left for the slabs); otherwise
     // each thread stores its 128-byte row directly
     const bool tma_ds = sm == smem_raw;
@@ -1397,22 +1398,44 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
             for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
                 uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
                 const float f = which == 0 ? 1.f : A.scale;
+                uint8_t* slab = slabs + (warp - 4) * 4096;
+                if (tma_ds) {  // the slab's previous bulk store (dS^T or dV) has been read
+                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                    __syncwarp();
+                }
 #pragma unroll 1
                 for (int c = 0; c < 2; ++c) {
                     float v[32];
                     ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
-                    uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
 #pragma unroll
-                    for (int k8 = 0; k8 < 4; ++k8)
-                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
-                                            pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
+                    for (int k8 = 0; k8 < 4; ++k8) {
+                        const uint4 q = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
+                                                   pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
+                        if (tma_ds)
+                            *reinterpret_cast<uint4*>(slab + lane * 128 + (((c * 4 + k8) ^ (lane & 7)) << 4)) = q;
+                        else
+                            reinterpret_cast<uint4*>(dst + c * 32)[k8] = q;
+                    }
+                }
+                if (tma_ds) {  // 32 key rows x 64 columns of dV / dK -> dqkv, one bulk tensor store
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) {
+                        const int col = (which == 0 ? 2 * A.h : A.h) + head * kHD + half * 64;
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                reinterpret_cast<uint64_t>(&tmdQKV)),
+                            "r"(smem_u32(slab)), "r"(col), "r"(b * A.s + kt * kT + quarter * 32)
+                            : "memory");
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
                 }
             }
             fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(acc_free));
         }
-        if (tma_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dS^T written
+        if (tma_ds && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // dS^T, dV, dK written
     }
     fence_before();
     __syncthreads();
@@ -1460,6 +1483,18 @@ bool probs_view(CUtensorMap* m, uint16_t* base, int s, int nh, int B) {
     cuuint32_t box[4] = {64, 32, 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Row-major [rows][cols] bf16 matrix, box 64 columns x 32 rows, SWIZZLE_128B (per-warp store slabs).
+bool rows_view(CUtensorMap* m, uint16_t* base, long long cols, long long rows) {
+    EncodeFn fn = encode();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, 32};
+    cuuint32_t es[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
               CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -1570,8 +1605,10 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
         e = set_smem(flash_bwd_t_kernel, smem, cfg3);
         if (e != cudaSuccess) return e;
         const int items = (s / kT) * nh * B;
+        CUtensorMap mdqkv;  // [B*s][3h] bf16, box 64 columns x 32 rows (the dV / dK slabs)
+        if (!rows_view(&mdqkv, dqkv, 3ll * h, (long long)B * s)) return cudaErrorInvalidValue;
         launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, mds,
-                  a);
+                  mdqkv, a);
         return launched(1);
     }
     if (variant == 0) {
