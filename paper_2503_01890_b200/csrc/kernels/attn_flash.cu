@@ -316,7 +316,7 @@ struct FwdItems {
 template <int kParts>
 __global__ void __launch_bounds__((4 + 4 * kParts) * 32, 1)
 flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const FwdParams A) {
+                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
     uint8_t* sQ = sm;              // [2] per item
@@ -339,6 +339,8 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     uint64_t* o_free = bar + 20;  // [2] softmax warps have drained an O buffer
     uint64_t* pv_done = bar + 22;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 23);
+    // O epilogue: per softmax warp a 32 x 32 bf16 slab (SWIZZLE_64B image) -> TMA bulk tensor store
+    uint8_t* slabs = sm + 6 * kTile + 1024;
     constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
     constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
     // statically shared (not carved from the aligned dynamic block) so the compiler emits LDS/STS
@@ -471,7 +473,8 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
         // its O buffer is complete by then and the stores overlap the next item's tensor work
         int pend_it = -1;
         float pend_inv = 0.f;
-        uint16_t* pend_row = nullptr;
+        int pend_col = 0, pend_row0 = 0;  // O column of this slice, first token row of the warp's 32 rows
+        uint8_t* slab = slabs + (warp - 4) * 2048;
         auto epilogue = [&]() {
             const int buf = pend_it & 1;
             mbar_wait(smem_u32(&o_full[buf]), (pend_it >> 1) & 1);
@@ -480,12 +483,31 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             for (int c = 0; c < kC / 32; ++c) {
                 float v[32];
                 ld32(tmem + lane_base + 256 + buf * 128 + part * kC + c * 32, v);
-                uint4* op = reinterpret_cast<uint4*>(pend_row + c * 32);
                 const float inv = pend_inv;
+                if constexpr (kParts != 2) {  // pk4 (A/B variant): no smem left for slabs
+                    uint4* op = reinterpret_cast<uint4*>(A.O + (size_t)(pend_row0 + lane) * A.h + pend_col + c * 32);
+#pragma unroll
+                    for (int k8 = 0; k8 < 4; ++k8)
+                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
+                                            pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+                    continue;
+                }
+                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slab free
+                __syncwarp();
 #pragma unroll
                 for (int k8 = 0; k8 < 4; ++k8)
-                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
-                                        pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+                    *reinterpret_cast<uint4*>(slab + lane * 64 + ((k8 ^ ((lane >> 1) & 3)) << 4)) =
+                        make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
+                                   pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                                     reinterpret_cast<uint64_t>(&tmO)),
+                                 "r"(smem_u32(slab)), "r"(pend_col + c * 32), "r"(pend_row0)
+                                 : "memory");
+                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                }
             }
             fence_before();
             __syncwarp();
@@ -580,9 +602,11 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             if (part == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
             pend_it = it;
             pend_inv = inv;
-            pend_row = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + part * kC;
+            pend_col = head * kHD + part * kC;
+            pend_row0 = b * A.s + qt * kT + quarter * 32;
         }
         if (pend_it >= 0) epilogue();
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // O written
     }
     fence_before();
     __syncthreads();
@@ -1487,15 +1511,16 @@ bool probs_view(CUtensorMap* m, uint16_t* base, int s, int nh, int B) {
 }
 
 // Row-major [rows][cols] bf16 matrix, box 64 columns x 32 rows, SWIZZLE_128B (per-warp store slabs).
-bool rows_view(CUtensorMap* m, uint16_t* base, long long cols, long long rows) {
+bool rows_view(CUtensorMap* m, uint16_t* base, long long cols, long long rows, int box_cols = 64,
+               CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeFn fn = encode();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-    cuuint32_t box[2] = {64, 32};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, 32};
     cuuint32_t es[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <typename K>
@@ -1559,19 +1584,22 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     }();
     const int items = (s / kT) * nh * B;
     const int grid = items < kNumSMs ? items : kNumSMs;
+    CUtensorMap mo;  // O [B*s][h], box 32 x 32, SWIZZLE_64B (the epilogue slabs)
+    if (!rows_view(&mo, O, h, (long long)B * s, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
+    // tiles | barriers (1 KB) | epilogue slabs (2 KB per softmax warp)
     if (parts == 2) {
-        const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
+        const size_t smem = 1024 + 6 * (size_t)kTile + 1024 + 8 * 2048;
         static bool cfg2 = false;
         cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
         if (e != cudaSuccess) return e;
-        launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, a);
+        launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, mo, a);
         return launched(1);
     }
     const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
     static bool cfg4 = false;
     cudaError_t e = set_smem(flash_fwd_pk_kernel<4>, smem, cfg4);
     if (e != cudaSuccess) return e;
-    flash_fwd_pk_kernel<4><<<grid, (4 + 16) * 32, smem, st>>>(mq, mk, mv, a);
+    flash_fwd_pk_kernel<4><<<grid, (4 + 16) * 32, smem, st>>>(mq, mk, mv, mo, a);
     return launched(1);
 }
 
