@@ -103,7 +103,7 @@ class GemmDesc(C.Structure):
     ]
 
 
-EPI_BIAS, EPI_GELU, EPI_RESIDUAL, EPI_AUX = 1, 2, 4, 16
+EPI_BIAS, EPI_GELU, EPI_RESIDUAL, EPI_AUX, EPI_GELU_BWD = 1, 2, 4, 16, 32
 CAUSAL_NONE, CAUSAL_SKIP_UPPER, CAUSAL_K_UPTO_M, CAUSAL_K_FROM_M = 0, 1, 2, 3
 
 _EXTRA_SIGS = {

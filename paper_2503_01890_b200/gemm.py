@@ -14,7 +14,7 @@ def _stream(stream):
 
 
 def gemm(a, b, c, *, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, bias=None, residual=None, aux=None,
-         gelu=False, causal=0, block_n=0, stream=None):
+         gelu=False, gelu_bwd=False, causal=0, block_n=0, stream=None):
     """c = epi(alpha * a @ b^T + beta * c) with logical a (M,K), b (N,K) — 2-D or 3-D (batch first).
 
     a_mn: `a` is given as its (K, M) storage (MN-major); same for b_mn with (K, N).
@@ -49,6 +49,8 @@ def gemm(a, b, c, *, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, bias=None, res
         d.aux, d.ld_aux, d.aux_s1 = x2.data_ptr(), x2.stride(1), x2.stride(0)
     if gelu:
         epi |= N.EPI_GELU
+    if gelu_bwd:  # c = (a @ b^T) * GELU'(aux): aux holds the pre-activation (read, not written)
+        epi = (epi & ~N.EPI_AUX) | N.EPI_GELU_BWD
     d.alpha, d.beta, d.epilogue, d.causal, d.block_n = alpha, beta, epi, causal, block_n
     N.check(N.lib().ah_gemm_bf16(C.byref(d), _stream(stream)), "ah_gemm_bf16")
     return c
