@@ -49,17 +49,26 @@ typedef struct ah_adam_hparams {
     int32_t step;       /* 1-based step used for bias correction */
 } ah_adam_hparams;
 
+/* Gradient statistics buffer: device float[AH_STATS_FLOATS], zeroed once by the caller.
+ * [0] = sum of squared unscaled grads, [1] = (uint32) count of non-finite grads, both
+ * ACCUMULATED over the launches that use the buffer, in stream order; the rest is scratch for
+ * the fixed-order cross-CTA reduction (bitwise reproducible: no float atomics). One buffer
+ * must not be used by two launches running concurrently. Zero [0] and [1] to restart. */
+#define AH_STATS_FLOATS 520
+
 /* Fused AdamW on one parameter span (one block = m_p params, workload.cpp:41-44):
  * fp32 master p / moments m, v updated in place from bf16 grads g scaled by inv_scale;
  * optional bf16 copy of the updated params into p_bf16 (may alias nothing else).
- * skip_flag: optional device int32; non-zero => no-op (overflow skip).
- * stats: optional device float[2] accumulated as {sum g^2, (uint32)non-finite count}.
+ * skip_flag: optional device int32; non-zero => no-op (overflow skip). Pointing it at
+ * stats + 1 of a preceding ah_grad_stats skips the update iff a grad was inf / nan.
+ * stats: optional AH_STATS_FLOATS buffer (above) accumulating the grads this launch reads.
  * 28 HBM bytes/param with p_bf16, 26 without. */
 int ah_adam_step(const ah_adam_hparams* hp, float* p, float* m, float* v, const uint16_t* g,
                  uint16_t* p_bf16, size_t n, float inv_scale, const int32_t* skip_flag,
                  float* stats, void* stream);
 
-/* Grad norm / overflow pre-pass (warp-shuffle reductions) into stats as above. */
+/* Grad norm / overflow pre-pass (2 B/param read; warp-shuffle + fixed-order cross-CTA
+ * reductions) accumulated into an AH_STATS_FLOATS buffer as above. */
 int ah_grad_stats(const uint16_t* g, size_t n, float inv_scale, float* stats, void* stream);
 
 /* bf16 materialisation of a GPU-resident fp32 master (paper footnote 2, PAPER.md:205-207;
@@ -231,6 +240,21 @@ typedef struct ah_trainer_stats {
      * of the copy lanes. hidden = 1 - blocked / (h2d + d2h busy). */
     double window_iters, compute_busy_ms, h2d_busy_ms, d2h_busy_ms, offload_blocked_ms;
     double h2d_gbps, d2h_gbps; /* achieved host-link bandwidth of the copy ops */
+    /* offload_blocked_ms split: time the compute lane waited while the needed copy was running
+     * (copy_blocked_ms) vs before it had started — held up upstream by the CPU optimizer or the
+     * copy lane's own order (upstream_blocked_ms). hidden = 1 - copy_blocked / (h2d + d2h busy). */
+    double copy_blocked_ms, upstream_blocked_ms;
+    double cpu_busy_ms; /* CpuOptim host time of the window's iterations */
+    double window_ms;   /* compute-stream span of the window (first op start -> last op end) */
+    double sim_steady_fifo_s, sim_steady_ps_s; /* reference scheduler, both orders of this plan */
+    int32_t priority_sched;                    /* order the executor currently runs */
+    /* Gradient statistics of the last drained iteration (this rank's gradients): global norm,
+     * non-finite count, and block groups whose update was skipped because a gradient was
+     * inf / nan (per-block overflow check: the pipelined schedule updates block L before block
+     * 1's gradients exist, so the skip is per block group, not per step). */
+    double grad_norm;
+    int64_t nonfinite_grads;
+    int32_t skipped_updates;
 } ah_trainer_stats;
 
 int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);
@@ -243,6 +267,9 @@ int ah_trainer_drain(void* trainer, float* loss);
 int ah_trainer_step(void* trainer, const int32_t* tokens, const int32_t* targets, float* loss);
 int ah_trainer_stats_get(void* trainer, ah_trainer_stats* out);
 int ah_trainer_reset_stats(void* trainer);
+/* Run subsequent iterations in the priority-based (1, paper §3.3) or FIFO (0) per-lane order of
+ * the reference scheduler (simulator.cpp:413-450) for the same plan; drains first. */
+int ah_trainer_set_schedule(void* trainer, int32_t priority_sched);
 /* Per-lane op order of one steady-state iteration as "LANE:OP_block" tokens. */
 int ah_trainer_schedule(void* trainer, char* buf, size_t cap);
 /* fp32 master parameters of block b (1..L), 0 = token embedding, -1 = positions,
@@ -273,6 +300,16 @@ typedef struct ah_hw_profile {
     double cpu_adam_rate;     /* params/s, host AdamW with cfg->cpu_threads */
 } ah_hw_profile;
 int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out);
+
+/* Host side of the profiler: the CpuOptim lane's roofline on this host. n params of pinned
+ * 14 B/param state (allocated and freed inside: a setup call); stream_gbps = best in-place pass
+ * over p/m/v (fp32) and g (bf16) with trivial arithmetic (the 28 B/param pattern of the host
+ * AdamW), adam_gbps / adam_params_per_s = ah_cpu_adam on the same buffers. */
+typedef struct ah_host_profile {
+    double stream_gbps, adam_gbps, adam_params_per_s;
+    int32_t threads;
+} ah_host_profile;
+int ah_profile_host(size_t n, int32_t nthreads, ah_host_profile* out);
 
 /* Instrumentation for the bench: kernels launched by this library so far, and live GEMM
  * timing (enable=1 starts recording; enable=0 stops and returns totals since enabling). */

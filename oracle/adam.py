@@ -78,10 +78,10 @@ def synth(n, seed=7, scale=1.0, nonfinite=False):
     """SURVEY.md §8(d) synthetic Adam inputs: p~N(0,.02), m~N(0,1e-3), v=N(0,1e-3)^2,
     bf16 g~N(0,1e-2)*scale (+1 inf, 1 nan when nonfinite)."""
     rng = np.random.default_rng(seed)
-    p = rng.normal(0, 0.02, n).astype(np.float32)
-    m = rng.normal(0, 1e-3, n).astype(np.float32)
-    v = (rng.normal(0, 1e-3, n) ** 2).astype(np.float32)
-    g = (rng.normal(0, 1e-2, n) * scale).astype(np.float32)
+    p = rng.standard_normal(n, dtype=np.float32) * np.float32(0.02)
+    m = rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3)
+    v = np.square(rng.standard_normal(n, dtype=np.float32) * np.float32(1e-3))
+    g = rng.standard_normal(n, dtype=np.float32) * np.float32(1e-2 * scale)
     if nonfinite and n >= 2:
         idx = rng.choice(n, 2, replace=False)
         g[idx[0]] = np.inf

@@ -33,20 +33,28 @@ typedef struct {
     int32_t step;
 } oracle_adam_hparams;
 
-static float bf16_to_f32(uint16_t b) {
+static inline float bf16_to_f32(uint16_t b) {
     uint32_t u = (uint32_t)b << 16;
     float f;
     memcpy(&f, &u, 4);
     return f;
 }
 
-uint16_t oracle_f32_to_bf16(float f) {
+/* round-to-nearest-even; NaN -> quiet NaN with the payload's top bits (branch-free select) */
+static inline uint16_t f32_to_bf16(float f) {
     uint32_t u;
     memcpy(&u, &f, 4);
-    if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
-    return (uint16_t)((u + 0x7fffu + ((u >> 16) & 1u)) >> 16);
+    const uint32_t qnan = (u >> 16) | 0x40u;
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    return (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? qnan : rne);
 }
 
+uint16_t oracle_f32_to_bf16(float f) { return f32_to_bf16(f); }
+
+/* AVX-512 (x86-64-v4) and baseline clones, picked at load time: the timed CPU baseline is the
+ * vectorised restatement BASELINE.md §3 asks for. Vectorisation does not change a result:
+ * IEEE +,*,/,sqrt per element, no contraction, no reassociation (no -ffast-math). */
+__attribute__((target_clones("arch=x86-64-v4", "default")))
 void oracle_adam_f32(const oracle_adam_hparams* hp, float* p, float* m, float* v,
                      const uint16_t* g, uint16_t* out, size_t n, float inv_scale) {
     const double lr = hp->lr, b1 = hp->beta1, b2 = hp->beta2, wd = hp->weight_decay;
@@ -57,18 +65,27 @@ void oracle_adam_f32(const oracle_adam_hparams* hp, float* p, float* m, float* v
     const float step_size = (float)(lr / (1.0 - pow(b1, t)));
     const float inv_sqrt_bc2 = (float)(1.0 / sqrt(1.0 - pow(b2, t)));
     const float eps = hp->eps;
-    for (size_t i = 0; i < n; ++i) {
-        const float gf = bf16_to_f32(g[i]) * inv_scale;
-        float pi = p[i] * decay;
-        const float mi = beta1 * m[i] + omb1 * gf;
-        const float vi = beta2 * v[i] + omb2 * (gf * gf);
-        const float denom = sqrtf(vi) * inv_sqrt_bc2 + eps;
-        pi = pi - step_size * (mi / denom);
-        p[i] = pi;
-        m[i] = mi;
+#define ADAM_BODY                                                   \
+        const float gf = bf16_to_f32(g[i]) * inv_scale;             \
+        float pi = p[i] * decay;                                     \
+        const float mi = beta1 * m[i] + omb1 * gf;                   \
+        const float vi = beta2 * v[i] + omb2 * (gf * gf);            \
+        const float denom = sqrtf(vi) * inv_sqrt_bc2 + eps;          \
+        pi = pi - step_size * (mi / denom);                          \
+        p[i] = pi;                                                   \
+        m[i] = mi;                                                   \
         v[i] = vi;
-        if (out) out[i] = oracle_f32_to_bf16(pi);
+    if (out) {
+        for (size_t i = 0; i < n; ++i) {
+            ADAM_BODY
+            out[i] = f32_to_bf16(pi);
+        }
+    } else {
+        for (size_t i = 0; i < n; ++i) {
+            ADAM_BODY
+        }
     }
+#undef ADAM_BODY
 }
 
 /* Same rule evaluated in double (torch-style formula: division by sqrt(bc2)) — used only to
@@ -105,7 +122,7 @@ void oracle_grad_stats(const uint16_t* g, size_t n, float inv_scale, double* sum
 }
 
 void oracle_cast_f32_bf16(const float* src, uint16_t* dst, size_t n) {
-    for (size_t i = 0; i < n; ++i) dst[i] = oracle_f32_to_bf16(src[i]);
+    for (size_t i = 0; i < n; ++i) dst[i] = f32_to_bf16(src[i]);
 }
 
 /* Multi-threaded copy of oracle_adam_f32 for the timed CPU baseline (bench.py cpu_baseline

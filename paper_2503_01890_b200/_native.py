@@ -147,6 +147,10 @@ class TrainerStats(C.Structure):
         ("window_iters", C.c_double), ("compute_busy_ms", C.c_double), ("h2d_busy_ms", C.c_double),
         ("d2h_busy_ms", C.c_double), ("offload_blocked_ms", C.c_double), ("h2d_gbps", C.c_double),
         ("d2h_gbps", C.c_double),
+        ("copy_blocked_ms", C.c_double), ("upstream_blocked_ms", C.c_double), ("cpu_busy_ms", C.c_double),
+        ("window_ms", C.c_double), ("sim_steady_fifo_s", C.c_double), ("sim_steady_ps_s", C.c_double),
+        ("priority_sched", C.c_int32), ("grad_norm", C.c_double), ("nonfinite_grads", C.c_int64),
+        ("skipped_updates", C.c_int32),
     ]
 
 
@@ -171,7 +175,14 @@ class HwProfile(C.Structure):
                 ("gpu_adam_rate", C.c_double), ("cpu_adam_rate", C.c_double)]
 
 
+class HostProfile(C.Structure):
+    _fields_ = [("stream_gbps", C.c_double), ("adam_gbps", C.c_double), ("adam_params_per_s", C.c_double),
+                ("threads", C.c_int32)]
+
+
 _EXTRA_SIGS.update({
+    "ah_trainer_set_schedule": ([C.c_void_p, C.c_int32], C.c_int),
+    "ah_profile_host": ([C.c_size_t, C.c_int32, C.POINTER(HostProfile)], C.c_int),
     "ah_trainer_timer": ([C.c_void_p, C.c_int32, C.POINTER(C.c_float)], C.c_int),
     "ah_profile_block": ([C.POINTER(TrainerConfig), C.POINTER(HwProfile)], C.c_int),
     "ah_kernel_launches": ([], C.c_int64),

@@ -1,7 +1,9 @@
 // extern "C" boundary: optimizer, cast and host-link entry points (include/autohete.h).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <omp.h>
 #include <stdexcept>
 #include <string>
 
@@ -13,6 +15,7 @@
 namespace ah {
 void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uint16_t* g,
               uint16_t* p_bf16, std::size_t n, float inv_scale, int nthreads);
+double host_stream_gbps(float* p, float* m, float* v, uint16_t* g, std::size_t n, int nthreads, int reps);
 }
 
 namespace ah {
@@ -35,7 +38,7 @@ using ah::set_error;
 extern "C" {
 
 const char* ah_last_error(void) { return ah::g_last_error.c_str(); }
-int ah_abi_version(void) { return 3; }
+int ah_abi_version(void) { return 4; }
 
 int ah_adam_step(const ah_adam_hparams* hp, float* p, float* m, float* v, const uint16_t* g,
                  uint16_t* p_bf16, size_t n, float inv_scale, const int32_t* skip_flag,
@@ -118,6 +121,45 @@ int ah_stream_create(void** stream, int high_priority) {
     *stream = s;
     return AH_OK;
 }
+int ah_profile_host(size_t n, int32_t nthreads, ah_host_profile* out) {
+    if (!out || n == 0) return set_error(AH_ERR_INVALID, "ah_profile_host: bad argument");
+    if (nthreads <= 0) nthreads = omp_get_num_procs();
+    float *p = nullptr, *m = nullptr, *v = nullptr;
+    uint16_t* g = nullptr;
+    cudaError_t e = cudaHostAlloc((void**)&p, n * 4, cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&m, n * 4, cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&v, n * 4, cudaHostAllocPortable);
+    if (e == cudaSuccess) e = cudaHostAlloc((void**)&g, n * 2, cudaHostAllocPortable);
+    int rc = AH_OK;
+    if (e != cudaSuccess) {
+        rc = cuda_status(e, "ah_profile_host: cudaHostAlloc");
+    } else {
+#pragma omp parallel for schedule(static) num_threads(nthreads)
+        for (size_t i = 0; i < n; ++i) {
+            p[i] = 0.01f;
+            m[i] = 0.f;
+            v[i] = 0.f;
+            g[i] = 0x3c00;
+        }
+        out->threads = nthreads;
+        out->stream_gbps = ah::host_stream_gbps(p, m, v, g, n, nthreads, 4);
+        ah_adam_hparams hp{1e-4f, 0.9f, 0.999f, 1e-8f, 0.01f, 1};
+        ah::cpu_adam(hp, p, m, v, g, g, n, 1.f, nthreads);  // warm
+        double best = 1e30;
+        for (int r = 0; r < 3; ++r) {
+            hp.step = r + 2;
+            const double t0 = omp_get_wtime();
+            ah::cpu_adam(hp, p, m, v, g, g, n, 1.f, nthreads);
+            best = std::min(best, omp_get_wtime() - t0);
+        }
+        out->adam_params_per_s = (double)n / best;
+        out->adam_gbps = 28.0 * (double)n / best / 1e9;
+    }
+    for (void* q : {(void*)p, (void*)m, (void*)v, (void*)g})
+        if (q) cudaFreeHost(q);
+    return rc;
+}
+
 int ah_stream_destroy(void* stream) {
     return cuda_status(cudaStreamDestroy(static_cast<cudaStream_t>(stream)), "cudaStreamDestroy");
 }

@@ -18,7 +18,8 @@ extern "C" int ah_gemm_bf16(const ah_gemm_desc* d, void* stream) {
     g.block_n = d->block_n;
     if ((g.epilogue & AH_EPI_BIAS) && !g.bias) return ah::set_error(AH_ERR_INVALID, "ah_gemm_bf16: bias missing");
     if ((g.epilogue & AH_EPI_RESIDUAL) && !g.residual) return ah::set_error(AH_ERR_INVALID, "ah_gemm_bf16: residual missing");
-    if ((g.epilogue & AH_EPI_AUX) && !g.aux) return ah::set_error(AH_ERR_INVALID, "ah_gemm_bf16: aux missing");
+    if ((g.epilogue & (AH_EPI_AUX | AH_EPI_GELU_BWD)) && !g.aux)
+        return ah::set_error(AH_ERR_INVALID, "ah_gemm_bf16: aux missing (AH_EPI_AUX / AH_EPI_GELU_BWD read it)");
     return ah::cuda_status(ah::gemm::run(g, static_cast<cudaStream_t>(stream)), "ah_gemm_bf16");
 }
 

@@ -81,7 +81,12 @@ int ah_trainer_stats_get(void* tr, ah_trainer_stats* out) {
 
 int ah_trainer_reset_stats(void* tr) {
     if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
-    return AH_OK;
+    return guarded([&] { T(tr)->reset_stats(); });
+}
+
+int ah_trainer_set_schedule(void* tr, int32_t priority_sched) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    return guarded([&] { T(tr)->set_schedule(priority_sched != 0); });
 }
 
 int ah_trainer_schedule(void* tr, char* buf, size_t cap) {

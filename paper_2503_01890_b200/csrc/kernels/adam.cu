@@ -2,18 +2,21 @@
 // proj/core/src/simulator.cpp:217-226, duration model workload.cpp:71).
 //
 // One pass over HBM per parameter: read bf16 grad (2 B) + fp32 master/m/v (12 B), write
-// fp32 master/m/v (12 B) + bf16 working copy (2 B) = 28 algorithmic bytes/param. 128-bit
-// vector loads/stores (8 params per vector step), two steps in flight per thread, grid sized
-// to 4 resident CTAs x 148 SMs with a grid-stride loop. Grad unscale is fused; optional
-// by-product statistics (sum of squared unscaled grads, count of non-finite grads) are
-// reduced with warp shuffles, one atomic pair per CTA. An optional device-side skip flag
-// turns the launch into a no-op (dynamic loss-scaling overflow skip).
+// fp32 master/m/v (12 B) + bf16 working copy (2 B) = 28 algorithmic bytes/param. The default
+// kernel (adam_tma_kernel) is a persistent CTA per SM fed by a TMA bulk-copy ring; the
+// register-streaming adam_vec_kernel serves capped-grid launches. Grad unscale is fused;
+// optional statistics (sum of squared unscaled grads, count of non-finite grads) are reduced
+// with warp shuffles inside a CTA and across CTAs in a fixed order by the last CTA to finish
+// (stats_commit: no float atomics, so the result is bitwise reproducible). An optional device-
+// side skip flag turns the launch into a no-op (overflow skip; the executor points it at the
+// non-finite count of a grad_stats pre-pass).
 //
 // Arithmetic is IEEE round-to-nearest with no contraction (explicit __f*_rn), in exactly
 // the order of oracle/adam_oracle.c and csrc/runtime/cpu_adam.cpp, so the GPU result is
 // bit-identical to both CPU implementations.
 #include <cstdlib>
 
+#include "autohete.h"
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -50,6 +53,56 @@ __device__ __forceinline__ float adam_one(float& p, float& m, float& v, float g,
 __device__ __forceinline__ void account(Stat& st, float g) {
     st.sumsq = __fadd_rn(st.sumsq, __fmul_rn(g, g));
     st.nonfinite += isfinite(g) ? 0u : 1u;
+}
+
+// Statistics buffer (AH_STATS_FLOATS floats, include/autohete.h): [0] sum g^2, [1] (uint32)
+// non-finite count — both accumulated across launches in stream order — [2] (uint32) ticket,
+// [4 + 2c], [5 + 2c] the partials of CTA c. Called by one thread per CTA with the CTA total:
+// the CTA that takes the last ticket sums every partial in CTA order, adds the launch total to
+// [0]/[1] and re-arms the ticket, so the result does not depend on CTA completion order.
+constexpr int kStatsMaxCtas = 256;
+static_assert(4 + 2 * kStatsMaxCtas <= AH_STATS_FLOATS, "stats scratch");
+__device__ __forceinline__ void stats_commit(float* stats, float sum, unsigned bad) {
+    float* part = stats + 4;
+    unsigned* ticket = reinterpret_cast<unsigned*>(stats + 2);
+    __stcg(part + 2 * blockIdx.x, sum);
+    __stcg(reinterpret_cast<unsigned*>(part) + 2 * blockIdx.x + 1, bad);
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    if (t != gridDim.x - 1) return;
+    __threadfence();
+    float s = 0.f;
+    unsigned b = 0;
+    for (unsigned c = 0; c < gridDim.x; ++c) {
+        s = __fadd_rn(s, __ldcg(part + 2 * c));
+        b += __ldcg(reinterpret_cast<const unsigned*>(part) + 2 * c + 1);
+    }
+    stats[0] = __fadd_rn(stats[0], s);
+    reinterpret_cast<unsigned*>(stats)[1] += b;
+    *ticket = 0u;
+    __threadfence();
+}
+
+// CTA reduction (256 threads) in warp order, then stats_commit.
+__device__ __forceinline__ void block_stats_commit(float* stats, const Stat& st) {
+    __shared__ float s_sum[8];
+    __shared__ unsigned s_bad[8];
+    const float ws = warp_sum(st.sumsq);
+    const unsigned wb = warp_sum_u(st.nonfinite);
+    if ((threadIdx.x & 31) == 0) {
+        s_sum[threadIdx.x >> 5] = ws;
+        s_bad[threadIdx.x >> 5] = wb;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float a = 0.f;
+        unsigned b = 0;
+        for (unsigned w = 0; w < (blockDim.x >> 5); ++w) {
+            a = __fadd_rn(a, s_sum[w]);
+            b += s_bad[w];
+        }
+        stats_commit(stats, a, b);
+    }
 }
 
 constexpr int kThreads = 256;
@@ -134,10 +187,7 @@ adam_vec_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict_
             unsigned b = threadIdx.x < kThreads / 32 ? s_bad[threadIdx.x] : 0u;
             a = warp_sum(a);
             b = warp_sum_u(b);
-            if (threadIdx.x == 0) {
-                atomicAdd(stats, a);
-                if (b) atomicAdd(reinterpret_cast<unsigned*>(stats + 1), b);
-            }
+            if (threadIdx.x == 0) stats_commit(stats, a, b);
         }
     }
 }
@@ -266,10 +316,7 @@ adam_tma_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict_
             unsigned b = threadIdx.x < kConsumerWarps ? s_bad[threadIdx.x] : 0u;
             a = warp_sum(a);
             b = warp_sum_u(b);
-            if (threadIdx.x == 0) {
-                atomicAdd(stats, a);
-                if (b) atomicAdd(reinterpret_cast<unsigned*>(stats + 1), b);
-            }
+            if (threadIdx.x == 0) stats_commit(stats, a, b);
         }
     }
 }
@@ -291,14 +338,7 @@ __global__ void adam_scalar_kernel(float* p, float* m, float* v, const uint16_t*
         v[i] = vq;
         if (pout) pout[i] = (uint16_t)f32_to_bf16_bits(pp);
     }
-    if (stats) {
-        const float ws = warp_sum(st.sumsq);
-        const unsigned wb = warp_sum_u(st.nonfinite);
-        if ((threadIdx.x & 31) == 0) {
-            atomicAdd(stats, ws);
-            if (wb) atomicAdd(reinterpret_cast<unsigned*>(stats + 1), wb);
-        }
-    }
+    if (stats) block_stats_commit(stats, st);
 }
 
 __global__ void cast_f32_bf16_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst,
@@ -335,12 +375,7 @@ __global__ void grad_stats_kernel(const uint16_t* __restrict__ g, size_t n, floa
     }
     for (size_t i = n_vec * 8 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
         account(st, __fmul_rn(bf16_bits_to_f32(g[i]), inv_scale));
-    const float a = warp_sum(st.sumsq);
-    const unsigned b = warp_sum_u(st.nonfinite);
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(stats, a);
-        if (b) atomicAdd(reinterpret_cast<unsigned*>(stats + 1), b);
-    }
+    block_stats_commit(stats, st);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
@@ -397,6 +432,7 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
         } else if (n_vec) {
             int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
             if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
+            if (a.stats && grid > kStatsMaxCtas) grid = kStatsMaxCtas;
             if (a.p_bf16 && a.stats)
                 adam_vec_kernel<true, true><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
             else if (a.p_bf16)
@@ -409,7 +445,8 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
         done = n_vec * 8;
     }
     if (done < a.n) {
-        const int grid = vec ? 1 : grid_for(a.n, 256, 4);
+        int grid = vec ? 1 : grid_for(a.n, 256, 4);
+        if (a.stats && grid > kStatsMaxCtas) grid = kStatsMaxCtas;
         adam_scalar_kernel<<<grid, 256, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, done, a.n, k,
                                                       a.skip, a.stats);
     }
@@ -432,8 +469,9 @@ cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, floa
                               cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     const bool vec = aligned16(g);
-    grad_stats_kernel<<<grid_for(vec ? n / 8 + 1 : n, 256, 8), 256, 0, stream>>>(g, n, inv_scale,
-                                                                               stats, vec);
+    int grid = grid_for(vec ? n / 8 + 1 : n, 256, 8);
+    if (grid > kStatsMaxCtas) grid = kStatsMaxCtas;
+    grad_stats_kernel<<<grid, 256, 0, stream>>>(g, n, inv_scale, stats, vec);
     return launched(1);
 }
 

@@ -720,6 +720,26 @@ cudaError_t token_index(const int* tok, int T, int* uniq, int* offs, int* pos, i
     return launched(1);
 }
 
+namespace {
+// Ids outside [0, V) would index wte / dwte / the logits row out of bounds: flag them (integer
+// atomicOr, deterministic) and replace them by 0 in the executor's own device copy.
+__global__ void sanitize_ids_kernel(int* __restrict__ ids, int n, int V, int* __restrict__ flag) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int x = ids[i];
+    if (x < 0 || x >= V) {
+        ids[i] = 0;
+        atomicOr(flag, 1);
+    }
+}
+}  // namespace
+
+cudaError_t sanitize_ids(int* ids, int n, int V, int* flag, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    sanitize_ids_kernel<<<(n + 255) / 256, 256, 0, st>>>(ids, n, V, flag);
+    return launched(1);
+}
+
 cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* offs, const int* pos,
                               const int* n_uniq, int T, float* dwte, int h, cudaStream_t st) {
     embed_bwd_tok_dev_kernel<<<T, 256, 0, st>>>(dx, uniq, offs, pos, n_uniq, dwte, h);

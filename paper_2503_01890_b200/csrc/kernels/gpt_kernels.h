@@ -93,6 +93,8 @@ namespace gpt {
 // sorts (token, position) pairs (single CTA bitonic sort, T <= 16384) and emits
 // uniq[n_uniq], offs[n_uniq + 1], pos[T] and *n_uniq. Buffers: ints of T, T+1, T, 1.
 cudaError_t token_index(const int* tok, int T, int* uniq, int* offs, int* pos, int* n_uniq, cudaStream_t st);
+// ids in [0, V) are kept; any other id is replaced by 0 and sets *flag (device int) to 1.
+cudaError_t sanitize_ids(int* ids, int n, int V, int* flag, cudaStream_t st);
 // embedding scatter using the device-side count (grid = T, CTAs beyond n_uniq exit)
 cudaError_t embed_bwd_tok_dev(const uint16_t* dx, const int* uniq, const int* offs, const int* pos,
                               const int* n_uniq, int T, float* dwte, int h, cudaStream_t st);

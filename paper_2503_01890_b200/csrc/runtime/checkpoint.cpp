@@ -54,7 +54,11 @@ struct CheckpointIO {
                     throw std::runtime_error("checkpoint: bad magic");
                 if (std::fread(h2, 4, 9, f) != 9 || std::fread(&pb, 8, 1, f) != 1)
                     throw std::runtime_error("checkpoint: truncated header");
-                if (std::memcmp(h2, hdr, 8 * 4) != 0 || pb != per_block)
+                // shape + dp layout; the batch size (hdr[4]) does not enter the optimizer state
+                const int cmp[7] = {0, 1, 2, 3, 5, 6, 7};
+                bool same = pb == per_block;
+                for (int c : cmp) same = same && h2[c] == hdr[c];
+                if (!same)
                     throw std::invalid_argument("checkpoint: model shape / data-parallel layout mismatch");
                 if (t.submitted_ != 0) throw std::logic_error("checkpoint: load before the first iteration");
                 t.step_base_ = h2[8];

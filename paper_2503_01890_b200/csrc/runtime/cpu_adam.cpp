@@ -14,9 +14,7 @@
 #include <cstdint>
 #include <cstring>
 #include <cstdlib>
-#include <emmintrin.h>
 #include <omp.h>
-#include <xmmintrin.h>
 
 #include "adam_scalars.h"
 
@@ -58,63 +56,11 @@ inline void adam_loop(float* __restrict p, float* __restrict m, float* __restric
     }
 }
 
-// Same arithmetic, blocks of 64 params computed into registers / L1 and the bf16 output (the
-// buffer the next ParamPrefetch DMA reads) written with non-temporal 16-byte stores, so the
-// H2D copy that follows would find the data in DRAM instead of dirty in the CPU caches
-// (experiment; off by default, see cpu_adam below).
-constexpr std::size_t kNtBlock = 64;
-template <bool kNtAll>
-inline void adam_loop_nt(float* __restrict p, float* __restrict m, float* __restrict v,
-                         const uint16_t* __restrict g, uint16_t* __restrict out, std::size_t n,
-                         const AdamConsts& k, float inv_scale) {
-    alignas(64) float tp[kNtBlock], tm[kNtBlock], tv[kNtBlock];
-    alignas(64) uint16_t to[kNtBlock];
-    std::size_t i0 = 0;
-    for (; i0 + kNtBlock <= n; i0 += kNtBlock) {
-#pragma omp simd
-        for (std::size_t j = 0; j < kNtBlock; ++j) {
-            const std::size_t i = i0 + j;
-            const float gf = bf16_to_f32(g[i]) * inv_scale;
-            float pi = p[i] * k.decay;
-            const float mi = k.beta1 * m[i] + k.one_minus_beta1 * gf;
-            const float vi = k.beta2 * v[i] + k.one_minus_beta2 * (gf * gf);
-            const float denom = std::sqrt(vi) * k.inv_sqrt_bc2 + k.eps;
-            pi = pi - k.step_size * (mi / denom);
-            tp[j] = pi;
-            tm[j] = mi;
-            tv[j] = vi;
-            to[j] = f32_to_bf16(pi);
-        }
-        for (std::size_t j = 0; j < kNtBlock; j += 8)
-            _mm_stream_si128(reinterpret_cast<__m128i*>(out + i0 + j), _mm_load_si128(reinterpret_cast<const __m128i*>(to + j)));
-        if (kNtAll) {
-            for (std::size_t j = 0; j < kNtBlock; j += 4) {
-                _mm_stream_ps(p + i0 + j, _mm_load_ps(tp + j));
-                _mm_stream_ps(m + i0 + j, _mm_load_ps(tm + j));
-                _mm_stream_ps(v + i0 + j, _mm_load_ps(tv + j));
-            }
-        } else {
-            std::memcpy(p + i0, tp, sizeof(tp));
-            std::memcpy(m + i0, tm, sizeof(tm));
-            std::memcpy(v + i0, tv, sizeof(tv));
-        }
-    }
-    if (i0 < n) adam_loop<true>(p + i0, m + i0, v + i0, g + i0, out + i0, n - i0, k, inv_scale);
-    _mm_sfence();  // the streaming stores are globally visible before the lane signals completion
-}
-
 __attribute__((target_clones("arch=sapphirerapids", "arch=znver4", "avx2", "default")))
 void adam_span(float* __restrict p, float* __restrict m, float* __restrict v,
                const uint16_t* __restrict g, uint16_t* __restrict out, std::size_t n,
-               AdamConsts k, float inv_scale, int nt) {
-    const bool aligned = ((reinterpret_cast<std::uintptr_t>(p) | reinterpret_cast<std::uintptr_t>(m) |
-                           reinterpret_cast<std::uintptr_t>(v)) & 15u) == 0 &&
-                         (reinterpret_cast<std::uintptr_t>(out) & 15u) == 0;
-    if (out && nt == 2 && aligned)
-        adam_loop_nt<true>(p, m, v, g, out, n, k, inv_scale);
-    else if (out && nt == 1 && aligned)
-        adam_loop_nt<false>(p, m, v, g, out, n, k, inv_scale);
-    else if (out)
+               AdamConsts k, float inv_scale) {
+    if (out)
         adam_loop<true>(p, m, v, g, out, n, k, inv_scale);
     else
         adam_loop<false>(p, m, v, g, out, n, k, inv_scale);
@@ -126,21 +72,45 @@ void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uin
               uint16_t* p_bf16, std::size_t n, float inv_scale, int nthreads) {
     const AdamConsts k = derive_adam_scalars(hp);
     if (nthreads <= 0) nthreads = omp_get_num_procs();
-    // AH_CPU_ADAM_NT: 0 regular stores (default), 1 streaming bf16 output, 2 + streaming p/m/v.
-    // Measured on the 16-vCPU box (10B, 15 offloaded blocks): 1423 / 1512 / 1674 ms per step —
-    // streaming stores do not speed the following H2D DMA up, so they stay off.
-    static const int nt = [] {
-        const char* e = std::getenv("AH_CPU_ADAM_NT");
-        return e ? std::atoi(e) : 0;
-    }();
+    // (Non-temporal stores of the bf16 output / of p, m, v were measured slower on the 10B plan:
+    // 1512 / 1674 vs 1423 ms per step — the in-place update re-writes lines it just read.)
     constexpr std::size_t kChunk = 16384;  // 64 KiB of fp32 per stream per chunk
     const std::size_t n_chunks = (n + kChunk - 1) / kChunk;
 #pragma omp parallel for schedule(static) num_threads(nthreads) if (n_chunks > 1)
     for (std::size_t c = 0; c < n_chunks; ++c) {
         const std::size_t a = c * kChunk;
         const std::size_t len = (a + kChunk <= n) ? kChunk : n - a;
-        adam_span(p + a, m + a, v + a, g + a, p_bf16 ? p_bf16 + a : nullptr, len, k, inv_scale, nt);
+        adam_span(p + a, m + a, v + a, g + a, p_bf16 ? p_bf16 + a : nullptr, len, k, inv_scale);
     }
+}
+
+// Overflow-skip path of CpuOptim: the shared host buffer holds the block's gradients after
+// GradOffload; the next ParamPrefetch must find bf16(master) there again.
+void cpu_cast_f32_bf16(const float* src, uint16_t* dst, std::size_t n, int nthreads) {
+    if (nthreads <= 0) nthreads = omp_get_num_procs();
+#pragma omp parallel for simd schedule(static) num_threads(nthreads)
+    for (std::size_t i = 0; i < n; ++i) dst[i] = f32_to_bf16(src[i]);
+}
+
+// Host-DRAM roofline of CpuOptim (runtime profiler): the same in-place streams as the host
+// AdamW — fp32 p/m/v read + written, bf16 g read + written (28 B/param) — with trivial
+// arithmetic, over `nthreads` threads. Returns GB/s of the best of `reps` passes.
+double host_stream_gbps(float* p, float* m, float* v, uint16_t* g, std::size_t n, int nthreads, int reps) {
+    if (nthreads <= 0) nthreads = omp_get_num_procs();
+    double best = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        const double t0 = omp_get_wtime();
+#pragma omp parallel for simd schedule(static) num_threads(nthreads)
+        for (std::size_t i = 0; i < n; ++i) {
+            p[i] *= 0.999f;
+            m[i] *= 0.999f;
+            v[i] *= 0.999f;
+            g[i] ^= 1u;
+        }
+        const double dt = omp_get_wtime() - t0;
+        if (dt > 0 && 28.0 * (double)n / dt / 1e9 > best) best = 28.0 * (double)n / dt / 1e9;
+    }
+    return best;
 }
 
 }  // namespace ah

@@ -24,6 +24,7 @@ namespace ah {
 
 void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uint16_t* g, uint16_t* p_bf16,
               std::size_t n, float inv_scale, int nthreads);
+void cpu_cast_f32_bf16(const float* src, uint16_t* dst, std::size_t n, int nthreads);
 
 namespace {
 
@@ -118,12 +119,10 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     {
         const char* e = std::getenv("AH_PREFETCH_WEIGHTS");
         prefetch_mat_ = !(e && e[0] == '0');
-        const char* o = std::getenv("AH_OPT_SIDE_CTAS");  // experiment knob, off by default
-        opt_side_ctas_ = o ? std::atoi(o) : 0;
     }
+    check(cudaGetDevice(&device_), "get device");
     plan(cfg);
     allocate_and_init();
-    check(cudaGetDevice(&device_), "get device");
     for (int l = 0; l < 4; ++l) lanes_[l] = std::thread([this, l] { lane_main(l); });
 }
 
@@ -165,9 +164,10 @@ Trainer::~Trainer() {
                     (void*)wpe_m_, (void*)wpe_v_, (void*)lnf_, (void*)lnf_m_, (void*)lnf_v_, (void*)wte_b_,
                     (void*)wpe_b_, (void*)lnf_b_, (void*)dwte_, (void*)dwpe_, (void*)dwte_b_, (void*)dwpe_b_,
                     (void*)dlnf_b_, (void*)logits_, (void*)xf_, (void*)meanf_, (void*)rstdf_, (void*)losses_,
-                    (void*)loss_dev_, (void*)tok_dev_})
+                    (void*)loss_dev_, (void*)tok_dev_, (void*)gstats_dev_})
         if (p) cudaFree(p);
     if (loss_host_) cudaFreeHost(loss_host_);
+    if (gstats_host_) cudaFreeHost(gstats_host_);
     if (tok_host_) cudaFreeHost(tok_host_);
     cudaStreamDestroy(s_compute_);
     cudaStreamDestroy(s_h2d_);
@@ -236,17 +236,38 @@ void Trainer::plan(const ah_trainer_config& cfg) {
     }
     if (cfg.fine_tune) strategy_ = hetsim::fine_tune_prefetch(profile_, strategy_, hw_);
     sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    sim_steady_[ps_ ? 1 : 0] = sim_.steady_state_time;
+    try {  // the other schedule of the same plan, for the PS-vs-FIFO comparison
+        sim_steady_[ps_ ? 0 : 1] = hetsim::run(profile_, strategy_, hw_, 3, !ps_).steady_state_time;
+    } catch (const std::exception&) {
+        sim_steady_[ps_ ? 0 : 1] = std::nan("");
+    }
+    compile_order();
+}
+
+// Per-lane op order of iteration 1 and of the steady state (iteration 2) from the scheduler.
+void Trainer::compile_order() {
+    for (auto& it : order_)
+        for (auto& lane : it) lane.clear();
     for (const hetsim::CompletedOp& op : sim_.trace) {
         if (op.iter > 2) continue;
         order_[op.iter - 1][lane_of(op.kind)].push_back({(int)op.kind, op.block, op.backward_copy});
     }
 }
 
+void Trainer::set_schedule(bool priority) {
+    drain();  // every lane idle: the next iteration starts on the new order
+    if (priority == ps_) return;
+    ps_ = priority;
+    sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    compile_order();
+}
+
 // ---------------------------------------------------------------------------------------
 void Trainer::allocate_and_init() {
     const size_t T = d_.T(), h = d_.h, mp = d_.m_p();
     const BlockLayout lay = BlockLayout::make(h);
-    check(cudaDeviceGetDefaultMemPool(&pool_, 0), "mempool");
+    check(cudaDeviceGetDefaultMemPool(&pool_, device_), "mempool");  // this rank's GPU, not GPU 0
     uint64_t thr = UINT64_MAX;
     check(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
     if (const char* e = std::getenv("AH_POOL_INTERNAL_DEPS")) {  // experiment knob: 0 = never make a
@@ -277,10 +298,13 @@ void Trainer::allocate_and_init() {
     dalloc((void**)&logits_, T * (size_t)d_.Vp * 2);
     dalloc((void**)&xf_, T * h * 2);
     for (float** p : {&meanf_, &rstdf_, &losses_}) dalloc((void**)p, T * 4);
-    dalloc((void**)&loss_dev_, 256);
+    dalloc((void**)&loss_dev_, 256);  // [0] mean loss, [1] (int) out-of-range id flag
+    dalloc((void**)&gstats_dev_, (size_t)(d_.L + 1) * AH_STATS_FLOATS * 4);
     inv_words_ = 5 * T + 8;
     dalloc((void**)&tok_dev_, 2 * inv_words_ * 4);
     check(cudaHostAlloc((void**)&loss_host_, 64, cudaHostAllocPortable), "host alloc");
+    check(cudaHostAlloc((void**)&gstats_host_, (size_t)(d_.L + 1) * 8, cudaHostAllocPortable), "host alloc");
+    std::memset(gstats_host_, 0, (size_t)(d_.L + 1) * 8);
     check(cudaHostAlloc((void**)&tok_host_, 2 * 2 * T * 4, cudaHostAllocPortable), "host alloc");
 
     cudaStream_t st = s_compute_;
@@ -336,6 +360,8 @@ void Trainer::allocate_and_init() {
             check(cudaMemsetAsync(b.m2, 0, n * 4, st), "memset");
         }
     }
+    check(cudaMemsetAsync(loss_dev_, 0, 256, st), "memset");
+    check(cudaMemsetAsync(gstats_dev_, 0, (size_t)(d_.L + 1) * AH_STATS_FLOATS * 4, st), "memset");
     check(cudaStreamSynchronize(st), "sync");
     cudaFree(tmp);
     cudaFree(tmpb);
@@ -535,6 +561,10 @@ void Trainer::upload_inputs(Iter& it) {
     if (it.on_device) {
         check(cudaMemcpyAsync(dtok, it.tokens, T * 4, cudaMemcpyDeviceToDevice, s_compute_), "tokens");
         check(cudaMemcpyAsync(dtgt, it.targets, T * 4, cudaMemcpyDeviceToDevice, s_compute_), "targets");
+        // device inputs were not seen by the host check in submit(): ids outside [0, V) are
+        // replaced by 0 (no out-of-bounds embedding / logits access) and reported by drain()
+        int* flag = reinterpret_cast<int*>(loss_dev_ + 1);
+        check(gpt::sanitize_ids(dtok, 2 * (int)T, d_.V, flag, s_compute_), "sanitize ids");
     } else {
         check(cudaMemcpyAsync(dtok, it.tokens, T * 4, cudaMemcpyHostToDevice, s_compute_), "tokens");
         check(cudaMemcpyAsync(dtgt, it.targets, T * 4, cudaMemcpyHostToDevice, s_compute_), "targets");
@@ -563,7 +593,7 @@ void Trainer::head_forward_backward(Iter& it) {
     check(gemm::run(g, st), "logits");
     check(gpt::cross_entropy(logits_, dtgt, losses_, T, d_.V, d_.Vp, 1.f / T, st), "ce");
     check(gpt::mean_loss(losses_, T, loss_dev_, st), "loss");
-    check(cudaMemcpyAsync(loss_host_, loss_dev_, 4, cudaMemcpyDeviceToHost, st), "loss d2h");
+    check(cudaMemcpyAsync(loss_host_, loss_dev_, 8, cudaMemcpyDeviceToHost, st), "loss d2h");  // loss + id flag
     gemm::GemmArgs dg;  // dxf = dlogits . wte
     dg.M = T; dg.N = h; dg.K = d_.Vp;
     dg.A = logits_; dg.lda = d_.Vp; dg.B = wte_b_; dg.b_mn_major = 1; dg.ldb = h; dg.C = ws_.dln; dg.ldc = h;
@@ -601,10 +631,15 @@ void Trainer::embed_backward_and_update(Iter& it) {
     check(gpt::f32_to_bf16(dwpe_, dwpe_b_, nwpe, st), "cvt");
     const int step = (step_base_ + (int)it.k);
     const float inv = 1.f / (float)dp_size_;
+    // overflow check of the replicated group (slot 0): one skip flag for all three updates
+    grad_stats_pass(0, dwte_b_, nwte, st);
+    check(launch_grad_stats(dwpe_b_, nwpe, inv, gstats(0), st), "grad stats");
+    check(launch_grad_stats(dlnf_b_, 2 * (size_t)h, inv, gstats(0), st), "grad stats");
     AdamArgs a1 = adam_args(adam_, step, wte_, wte_m_, wte_v_, dwte_b_, wte_b_, nwte);
     AdamArgs a2 = adam_args(adam_, step, wpe_, wpe_m_, wpe_v_, dwpe_b_, wpe_b_, nwpe);
     AdamArgs a3 = adam_args(adam_, step, lnf_, lnf_m_, lnf_v_, dlnf_b_, lnf_b_, 2 * (size_t)h);
     a1.inv_scale = a2.inv_scale = a3.inv_scale = inv;
+    a1.skip = a2.skip = a3.skip = reinterpret_cast<const int*>(gstats(0) + 1);
     check(launch_adam(a1, st), "adam wte");
     check(launch_adam(a2, st), "adam wpe");
     check(launch_adam(a3, st), "adam lnf");
@@ -678,7 +713,10 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
                 side_after_compute();
                 if (full_len() > mp) check(cudaMemsetAsync(b.wbuf + mp, 0, (full_len() - mp) * 2, s_side_), "pad");
                 dp_reduce_grads(b.wbuf, s_side_);
+                grad_stats_pass(i, b.wbuf + off, shard_, s_side_);  // the reduced shard this rank updates
                 op.done_on_side = true;
+            } else {
+                grad_stats_pass(i, b.wbuf, mp, st);
             }
             if (i == 1) embed_backward_and_update(it);
             break;
@@ -687,17 +725,9 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             AdamArgs aa = dp_ ? adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf + off, nullptr, shard_)
                               : adam_args(adam_, (step_base_ + (int)it.k), b.master, b.m1, b.m2, b.wbuf, nullptr, mp);
             aa.inv_scale = 1.f / (float)dp_size_;
-            if (opt_side_ctas_ > 0) {  // experiment: the update overlaps the next backward on the side stream
-                side_after_compute();
-                aa.max_ctas = opt_side_ctas_;
-                check(launch_adam(aa, s_side_), "adam");
-                check(cudaFreeAsync(b.wbuf, s_side_), "free wbuf");
-                b.wbuf = nullptr;
-                op.done_on_side = true;
-            } else {
-                check(launch_adam(aa, st), "adam");
-                free_wbuf();
-            }
+            aa.skip = reinterpret_cast<const int*>(gstats(i) + 1);  // no-op if a grad of block i is inf / nan
+            check(launch_adam(aa, st), "adam");
+            free_wbuf();
             break;
         }
         default:
@@ -728,6 +758,9 @@ void Trainer::run_d2h(Iter& it, RtOp& op) {
     const size_t n = dp_ ? shard_ : d_.m_p();
     const uint16_t* src = dp_ ? b.wbuf + shard_ * (size_t)dp_rank_ : b.wbuf;
     check(cudaMemcpyAsync(b.host_bf16, src, n * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
+    // the block's overflow check rides along: the CPU lane reads it after this op completes
+    check(cudaMemcpyAsync(gstats_host_ + 2 * op.block, gstats(op.block), 8, cudaMemcpyDeviceToHost, s_d2h_),
+          "offload stats");
     check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
     b.wbuf = nullptr;
 }
@@ -738,8 +771,44 @@ void Trainer::run_cpu(Iter& it, RtOp& op) {
     hp.step = (step_base_ + (int)it.k);
     const auto t0 = Clock::now();
     const size_t n = dp_ ? shard_ : d_.m_p();
-    cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);
+    uint32_t bad = 0;
+    std::memcpy(&bad, gstats_host_ + 2 * op.block + 1, 4);
+    if (bad == 0) {
+        cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);
+    } else {  // overflow skip: state untouched; the shared buffer holds grads -> restore bf16(master)
+        cpu_cast_f32_bf16(b.master, b.host_bf16, n, cpu_threads_);
+    }
     op.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+}
+
+float* Trainer::gstats(int slot) const { return gstats_dev_ + (size_t)slot * AH_STATS_FLOATS; }
+
+// Zero the slot's accumulators and run the overflow / norm pre-pass (2 B/param read) on the
+// group's gradients; the slot's non-finite count then gates the group's update.
+void Trainer::grad_stats_pass(int slot, const uint16_t* g, size_t n, cudaStream_t st) {
+    check(cudaMemsetAsync(gstats(slot), 0, 8, st), "stats reset");
+    check(launch_grad_stats(g, n, 1.f / (float)dp_size_, gstats(slot), st), "grad stats");
+}
+
+// After a drain: norm / non-finite count / skipped groups of the last iteration (fixed slot
+// order; this rank's gradients — under DP its reduced shards plus the replicated group).
+void Trainer::collect_grad_stats() {
+    std::vector<float> h((size_t)(d_.L + 1) * 2);
+    check(cudaMemcpy2D(h.data(), 8, gstats_dev_, AH_STATS_FLOATS * 4, 8, (size_t)(d_.L + 1), cudaMemcpyDeviceToHost),
+          "grad stats d2h");
+    double ss = 0.0;
+    long long bad = 0;
+    int skipped = 0;
+    for (int i = 0; i <= d_.L; ++i) {
+        uint32_t nb = 0;
+        std::memcpy(&nb, &h[(size_t)i * 2 + 1], 4);
+        ss += (double)h[(size_t)i * 2];
+        bad += nb;
+        skipped += nb ? 1 : 0;
+    }
+    grad_norm_ = std::sqrt(ss);
+    nonfinite_ = bad;
+    skipped_ = skipped;
 }
 
 void Trainer::side_after_compute() {
@@ -811,6 +880,13 @@ void Trainer::dp_allreduce_bf16(uint16_t* p, size_t n, cudaStream_t st) {
 // Public
 // ---------------------------------------------------------------------------------------
 void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_device) {
+    if (!on_device) {  // host ids index wte / dwte / the logits rows: reject any outside [0, V)
+        const size_t T = d_.T();
+        for (size_t t = 0; t < T; ++t)
+            if (tokens[t] < 0 || tokens[t] >= d_.V || targets[t] < 0 || targets[t] >= d_.V)
+                throw std::invalid_argument("trainer: token / target id outside [0, vocab) at position " +
+                                            std::to_string(t));
+    }
     Iter* it = new Iter;
     {
         std::lock_guard<std::mutex> lk(mu_);
@@ -890,6 +966,7 @@ float Trainer::drain() {
     check(cudaStreamSynchronize(s_compute_), "sync");
     check(cudaStreamSynchronize(s_h2d_), "sync");
     check(cudaStreamSynchronize(s_d2h_), "sync");
+    check(cudaStreamSynchronize(s_side_), "sync");
     // accumulate GPU lane busy time of finished iterations
     {
         std::lock_guard<std::mutex> lk(mu_);
@@ -906,7 +983,17 @@ float Trainer::drain() {
             }
     }
     account_window();
+    collect_grad_stats();
     last_loss_ = *loss_host_;
+    int bad = 0;
+    std::memcpy(&bad, loss_host_ + 1, 4);
+    if (bad) {  // an on-device batch carried ids outside [0, V): they were trained as id 0
+        check(cudaMemsetAsync(loss_dev_ + 1, 0, 4, s_compute_), "clear id flag");
+        check(cudaStreamSynchronize(s_compute_), "sync");
+        std::memset(loss_host_ + 1, 0, 4);
+        throw std::invalid_argument("trainer: token / target id outside [0, vocab) in an on-device batch "
+                                    "(replaced by 0 in that iteration)");
+    }
     return last_loss_;
 }
 
@@ -970,6 +1057,16 @@ void Trainer::stats(ah_trainer_stats* s) {
     s->offload_blocked_ms = win_blocked_ms_;
     s->h2d_gbps = win_h2d_ms_ > 0 ? win_h2d_bytes_ / (win_h2d_ms_ * 1e6) : 0.0;
     s->d2h_gbps = win_d2h_ms_ > 0 ? win_d2h_bytes_ / (win_d2h_ms_ * 1e6) : 0.0;
+    s->copy_blocked_ms = win_copy_blocked_ms_;
+    s->upstream_blocked_ms = win_upstream_blocked_ms_;
+    s->cpu_busy_ms = win_cpu_ms_;
+    s->window_ms = win_span_ms_;
+    s->sim_steady_fifo_s = sim_steady_[0];
+    s->sim_steady_ps_s = sim_steady_[1];
+    s->priority_sched = ps_ ? 1 : 0;
+    s->grad_norm = grad_norm_;
+    s->nonfinite_grads = nonfinite_;
+    s->skipped_updates = skipped_;
 }
 
 std::string Trainer::trace_json() {
@@ -1117,13 +1214,24 @@ float Trainer::timer(bool stop) {
     return ms;
 }
 
+void Trainer::reset_stats() {
+    std::lock_guard<std::mutex> lk(mu_);
+    for (LaneStats& l : lane_stats_) l = LaneStats{};
+    win_iters_ = win_compute_ms_ = win_h2d_ms_ = win_d2h_ms_ = win_blocked_ms_ = 0;
+    win_h2d_bytes_ = win_d2h_bytes_ = 0;
+    win_copy_blocked_ms_ = win_upstream_blocked_ms_ = win_cpu_ms_ = win_span_ms_ = 0;
+}
+
 }  // namespace ah
 
 namespace ah {
 
 // Offload overlap of the drained window: for every compute op that depends on a copy-lane or
 // CPU op, the idle gap before it on the compute stream (previous compute op end -> its start)
-// is time the compute lane was blocked by offloading.
+// is time the compute lane was blocked by offloading. The gap is split at the start of the
+// copy it waited for: the part while that copy ran is copy-blocked (the host link did not keep
+// up), the part before it is upstream-blocked (the copy itself waited for the CPU optimizer or
+// for the copy lane's in-order queue).
 void Trainer::account_window() {
     std::lock_guard<std::mutex> lk(mu_);
     if (iters_.empty()) return;
@@ -1131,27 +1239,46 @@ void Trainer::account_window() {
     for (auto& kv : iters_.front()->ops)
         if (kv.second.kind == OpKind::Forward && kv.second.block == 1) origin = kv.second.t0;
     if (!origin) return;
+    auto span = [&](const RtOp& o, double& a, double& b) {
+        float x = 0, y = 0;
+        if (cudaEventElapsedTime(&x, origin, o.t0) != cudaSuccess) return false;
+        if (cudaEventElapsedTime(&y, origin, o.t1) != cudaSuccess) return false;
+        a = x;
+        b = y;
+        return true;
+    };
     struct Span {
         double a, b;
-        bool waits_offload;
+        bool waits;
+        double ca, cb;  // the awaited copy's span (latest-finishing offload dependency)
     };
     std::vector<Span> comp;
-    double h2d = 0, d2h = 0, hb = 0, db = 0;
+    double h2d = 0, d2h = 0, hb = 0, db = 0, cpu = 0;
     const double wbytes = 2.0 * (double)(dp_ ? shard_ : d_.m_p());
     for (Iter* it : iters_)
         for (auto& kv : it->ops) {
             RtOp& o = kv.second;
-            if (o.lane == kCpu) continue;
-            float a = 0, b = 0;
-            if (cudaEventElapsedTime(&a, origin, o.t0) != cudaSuccess) continue;
-            if (cudaEventElapsedTime(&b, origin, o.t1) != cudaSuccess) continue;
+            if (o.lane == kCpu) {
+                cpu += o.host_ms;
+                continue;
+            }
+            double a = 0, b = 0;
+            if (!span(o, a, b)) continue;
             if (o.lane == kCompute) {
-                bool w = false;
+                Span sp{a, b, false, 0, 0};
                 for (const auto& dp : o.deps) {
                     const int k = dp.second.kind;
-                    w |= k == (int)OpKind::ParamPrefetch || k == (int)OpKind::GradOffload || k == (int)OpKind::CpuOptim;
+                    if (k != (int)OpKind::ParamPrefetch && k != (int)OpKind::GradOffload && k != (int)OpKind::CpuOptim)
+                        continue;
+                    sp.waits = true;
+                    const RtOp* d = find(dp.first, dp.second);
+                    double ca = 0, cb = 0;
+                    if (d && d->lane != kCpu && span(*d, ca, cb) && cb >= sp.cb) {
+                        sp.ca = ca;
+                        sp.cb = cb;
+                    }
                 }
-                comp.push_back({a, b, w});
+                comp.push_back(sp);
             } else if (o.lane == kH2D) {
                 h2d += b - a;
                 if (blocks_[(size_t)o.block].o) hb += wbytes;
@@ -1161,16 +1288,25 @@ void Trainer::account_window() {
             }
         }
     std::sort(comp.begin(), comp.end(), [](const Span& x, const Span& y) { return x.a < y.a; });
-    double busy = 0, blocked = 0;
+    double busy = 0, copy_blocked = 0, upstream = 0;
     for (size_t i = 0; i < comp.size(); ++i) {
         busy += comp[i].b - comp[i].a;
-        if (i > 0 && comp[i].waits_offload) blocked += std::max(0.0, comp[i].a - comp[i - 1].b);
+        if (i == 0 || !comp[i].waits) continue;
+        const double g0 = comp[i - 1].b, g1 = comp[i].a;
+        if (g1 <= g0) continue;
+        const double c = std::max(0.0, std::min(g1, comp[i].cb) - std::max(g0, comp[i].ca));
+        copy_blocked += c;
+        upstream += (g1 - g0) - c;
     }
     win_iters_ = (double)iters_.size();
     win_compute_ms_ = busy;
     win_h2d_ms_ = h2d;
     win_d2h_ms_ = d2h;
-    win_blocked_ms_ = blocked;
+    win_blocked_ms_ = copy_blocked + upstream;
+    win_copy_blocked_ms_ = copy_blocked;
+    win_upstream_blocked_ms_ = upstream;
+    win_cpu_ms_ = cpu;
+    win_span_ms_ = comp.empty() ? 0.0 : comp.back().b - comp.front().a;
     win_h2d_bytes_ = hb;
     win_d2h_bytes_ = db;
 }

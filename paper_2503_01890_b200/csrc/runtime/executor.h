@@ -50,7 +50,11 @@ public:
     const hetsim::ModelProfile& profile() const { return profile_; }
     const GptDims& dims() const { return d_; }
     const hetsim::SimResult& simulated() const { return sim_; }
+    // Switch the per-lane order of subsequent iterations between the priority-based (paper §3.3)
+    // and the FIFO schedule of the reference scheduler (drains first; weights / state kept).
+    void set_schedule(bool priority);
     void stats(ah_trainer_stats* out);
+    void reset_stats();  // zero the lane busy-time counters and the offload window
     // fp32 master of block b (1-based; 0 = embedding wte, -1 = wpe, -2 = final LN) -> host.
     void read_master(int block, float* out, size_t n);
     size_t master_size(int block) const;
@@ -155,6 +159,8 @@ private:
     hetsim::Strategy strategy_;
     hetsim::dp::DpSpec dp_spec_;
     hetsim::SimResult sim_;
+    double sim_steady_[2] = {0.0, 0.0};  // reference scheduler steady state: [0] FIFO, [1] PS
+    void compile_order();                // order_ from sim_
     bool ps_ = true;
     ah_adam_hparams adam_{};
     unsigned long long seed_ = 1234;
@@ -166,7 +172,6 @@ private:
     cudaStream_t s_side_ = nullptr;
     cudaEvent_t ev_c2s_ = nullptr, ev_s2c_ = nullptr;  // reused: a wait binds to the latest record
     bool prefetch_mat_ = true;
-    int opt_side_ctas_ = 0;
     std::vector<BlockState> blocks_;  // index 1..L
     std::vector<uint16_t*> x_;        // residual stream x[0..L] (x[0] = embedding output)
     uint16_t* gx_[2] = {nullptr, nullptr};  // residual-gradient ping-pong
@@ -206,6 +211,19 @@ private:
     // offload-overlap accounting of the last drain (see ah_trainer_stats)
     double win_iters_ = 0, win_compute_ms_ = 0, win_h2d_ms_ = 0, win_d2h_ms_ = 0, win_blocked_ms_ = 0;
     double win_h2d_bytes_ = 0, win_d2h_bytes_ = 0;
+    double win_copy_blocked_ms_ = 0, win_upstream_blocked_ms_ = 0, win_cpu_ms_ = 0, win_span_ms_ = 0;
+    // Gradient statistics (overflow check + norm), one AH_STATS_FLOATS slot per block group:
+    // slot 0 = embedding / positions / final LN, slot i = block i. Each slot is zeroed and filled
+    // by the grad_stats pre-pass right after the group's backward; its non-finite count is the
+    // skip flag of that group's update (GPU: device flag; CPU: read from gstats_host_).
+    float* gstats_dev_ = nullptr;
+    float* gstats_host_ = nullptr;  // pinned: [2 * slot] = {sum g^2, (uint32) non-finite}
+    double grad_norm_ = 0.0;
+    long long nonfinite_ = 0;
+    int skipped_ = 0;
+    float* gstats(int slot) const;
+    void grad_stats_pass(int slot, const uint16_t* g, size_t n, cudaStream_t st);
+    void collect_grad_stats();
     void account_window();
 };
 

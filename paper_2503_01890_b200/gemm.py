@@ -49,6 +49,8 @@ def gemm(a, b, c, *, a_mn=False, b_mn=False, alpha=1.0, beta=0.0, bias=None, res
         d.aux, d.ld_aux, d.aux_s1 = x2.data_ptr(), x2.stride(1), x2.stride(0)
     if gelu:
         epi |= N.EPI_GELU
+    if gelu_bwd and aux is None:
+        raise ValueError("gemm(gelu_bwd=True) needs aux (the pre-activation)")
     if gelu_bwd:  # c = (a @ b^T) * GELU'(aux): aux holds the pre-activation (read, not written)
         epi = (epi & ~N.EPI_AUX) | N.EPI_GELU_BWD
     d.alpha, d.beta, d.epilogue, d.causal, d.block_n = alpha, beta, epi, causal, block_n

@@ -143,6 +143,13 @@ class Trainer:
         out["lane_ops"] = list(s.lane_ops)
         return out
 
+    def reset_stats(self) -> None:
+        N.check(N.lib().ah_trainer_reset_stats(self._h), "ah_trainer_reset_stats")
+
+    def set_schedule(self, priority: bool) -> None:
+        """Priority-based (True) or FIFO (False) per-lane order for the following iterations."""
+        N.check(N.lib().ah_trainer_set_schedule(self._h, int(priority)), "ah_trainer_set_schedule")
+
     def schedule(self) -> list[str]:
         n = N.lib().ah_trainer_schedule(self._h, None, 0)
         buf = C.create_string_buffer(n)
@@ -199,6 +206,14 @@ def profile_hardware(model: ModelConfig, cpu_threads: int = 0) -> dict:
     cfg.cpu_threads = cpu_threads
     out = N.HwProfile()
     N.check(N.lib().ah_profile_block(C.byref(cfg), C.byref(out)), "ah_profile_block")
+    return {f: getattr(out, f) for f, _ in out._fields_}
+
+
+def profile_host(n: int = 100_000_000, threads: int = 0) -> dict:
+    """Host side of the profiler: the CpuOptim lane's roofline (in-place 28 B/param stream) and
+    the host AdamW on the same pinned buffers."""
+    out = N.HostProfile()
+    N.check(N.lib().ah_profile_host(n, threads, C.byref(out)), "ah_profile_host")
     return {f: getattr(out, f) for f, _ in out._fields_}
 
 

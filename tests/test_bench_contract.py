@@ -44,3 +44,12 @@ def test_product_arm_contract(cuda_device, native):
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["cpu_baseline"]["value"] and d["cpu_baseline"]["cores"] >= 1
     assert d["adam"]["roofline"]["bound"] == "hbm"
+
+
+def test_bench_spawns_ranks():
+    """`bench.py --gpus 2` outside a torch.distributed launcher spawns 2 ranks itself (the
+    driver may call it either way); each rank checks WORLD_SIZE == --gpus (gloo here)."""
+    d = run_bench("--gpus", "2", "--launch-check", timeout=300)
+    assert d["launch_check"] and d["world"] == 2
+    assert sorted(r["rank"] for r in d["ranks"]) == [0, 1]
+    assert len({r["pid"] for r in d["ranks"]}) == 2

@@ -80,12 +80,15 @@ def run_plan(plan_kw, ps=True, steps=3, fc=False):
 
 
 def test_plans_give_bit_identical_training_state(cuda_device, native):
-    base_loss, base_state, _ = run_plan(PLANS[0])
+    base_loss, base_state, base_st = run_plan(PLANS[0])
+    assert base_st["skipped_updates"] == 0 and base_st["nonfinite_grads"] == 0
+    assert np.isfinite(base_st["grad_norm"]) and base_st["grad_norm"] > 0
     for plan in PLANS[1:]:
         for ps in (True, False):
             loss, state, st = run_plan(plan, ps=ps)
             assert (st["c_hat"], st["p_hat"], st["o_hat"]) == (plan["c_hat"], plan["p_hat"], plan["o_hat"])
             assert loss == base_loss, (plan, ps)
+            assert st["grad_norm"] == base_st["grad_norm"], (plan, ps)  # fixed-order reductions
             for a, b in zip(state, base_state):
                 assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (plan, ps)
 
@@ -170,3 +173,66 @@ def test_long_run_is_deterministic_and_finite(cuda_device, native):
     assert all(np.isfinite(runs[0])), runs[0]
     assert runs[0] == runs[1]
     assert runs[0][-1] < runs[0][0] - 0.5  # it learns
+
+
+def test_overflow_check_skips_every_update(cuda_device, native, tmp_path):
+    """A NaN in block 2's weights makes every gradient group non-finite: the per-block overflow
+    check (grad_stats pre-pass -> skip flag) must leave all optimizer state untouched — GPU
+    blocks, host-optimizer blocks (whose shared buffer is restored to bf16(master)) and the
+    embedding group — and report the skips."""
+    import struct
+    from paper_2503_01890_b200.trainer import PlanConfig
+    L, h = MODEL["num_blocks"], MODEL["hidden"]
+    mp = 12 * h * h + 13 * h
+    plan = PlanConfig(fine_tune=False, gpu_mem_budget=1 << 40, c_hat=1, p_hat=1, o_hat=2)  # blocks 3, 4 on the CPU
+    tr = make(plan=plan)
+    tr.step(*batch(0))
+    path = str(tmp_path / "a.bin")
+    tr.save(path)
+    tr.close()
+    raw = bytearray(open(path, "rb").read())
+    hdr = 8 + 9 * 4 + 8
+    off = hdr + 3 * mp * 4 + 100 * 4  # block 2 master, element 100 (W_qkv)
+    raw[off:off + 4] = struct.pack("<f", float("nan"))
+    open(path, "wb").write(bytes(raw))
+    tr = make(plan=plan)
+    tr.load(path)
+    for k in range(2):
+        loss = tr.step(*batch(k + 1))
+    st = tr.stats()
+    assert not np.isfinite(loss)
+    assert st["skipped_updates"] == L + 1 and st["nonfinite_grads"] > 0
+    out = str(tmp_path / "b.bin")
+    tr.save(out)
+    tr.close()
+    after = open(out, "rb").read()
+    assert after[hdr:] == bytes(raw[hdr:])  # every master / m / v bit-identical
+
+
+def test_set_schedule_switches_to_fifo(cuda_device, native):
+    """PS for 2 iterations, then FIFO on the same trainer: the realised lane order follows the
+    FIFO scheduler and the training state equals the all-GPU plan's (order-invariant)."""
+    from paper_2503_01890_b200.trainer import PlanConfig
+    base_loss, base_state, _ = run_plan(PLANS[0], steps=4)
+    tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=4, priority_sched=True, fine_tune=False,
+                              gpu_mem_budget=1 << 40))
+    st = tr.stats()
+    assert st["priority_sched"] == 1 and st["sim_steady_ps_s"] > 0 and st["sim_steady_fifo_s"] > 0
+    for k in range(2):
+        tr.submit(*batch(k))
+    tr.set_schedule(False)
+    for k in range(2, 4):
+        tr.submit(*batch(k))
+    loss = tr.drain()
+    assert tr.stats()["priority_sched"] == 0
+    fifo_sched = tr.schedule()
+    trace = tr.trace()
+    for lane in ("COMPUTE", "H2D", "D2H"):
+        want = [t.split(":")[1].rstrip("b") for t in fifo_sched if t.startswith(lane + ":")]
+        got = [e["name"] for e in trace if e["cat"] == lane]
+        assert got[-len(want):] == want, lane
+    state = [tr.master(i).copy() for i in range(-2, MODEL["num_blocks"] + 1)]
+    tr.close()
+    assert loss == base_loss[-1]
+    for a, b in zip(state, base_state):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
