@@ -373,6 +373,7 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
     launches = N.lib().ah_kernel_launches() - L0
     st_t = tr.stats()  # lanes over the timed region; offload window = its last iterations
     loss = tr.drain()
+    _, mem_peak = tr.memory_csv()  # measured timeline of the window (reference CSV schema)
     value = T * steps * world / (ms_max / 1e3)
 
     # ---- GEMM window: CUDA events around every GEMM launch (an event between two kernels costs
@@ -470,6 +471,14 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
                  "h2d_bytes_per_step": st["h2d_bytes"], "d2h_bytes_per_step": st["d2h_bytes"],
                  "gpu_budget_gib": budget_gib},
         "offload": offload,
+        "lanes_vs_sim": {"measured_ms_per_step": lanes,
+                         "simulated_ms_per_step": dict(zip(("compute", "h2d", "d2h", "cpu_optim"),
+                                                           st_t["sim_lane_busy_ms"])),
+                         "note": "simulated = reference scheduler durations from the measured rates "
+                                 "(steady-state iteration of hetsim::run)"},
+        "memory": {"measured_peak_gib": mem_peak / 2**30, "simulated_peak_gib": st["simulated_peak_bytes"] / 2**30,
+                   "eq1_gib": st["modeled_peak_bytes"] / 2**30,
+                   "source": "Trainer.memory_csv(): persistent + stream-ordered transient buffers at op start / end"},
         "ps_gain": ps_gain,
         "grad": {"norm": st_t["grad_norm"], "nonfinite": st_t["nonfinite_grads"],
                  "skipped_updates": st_t["skipped_updates"]},
@@ -572,8 +581,8 @@ def main():
                           "tens of GB >> 126 MB L2"),
     }
     for k in ("e2e", "gpu_launches", "roofline", "model_flops_per_token", "mfu_model", "loss", "bound_by",
-              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "ps_gain", "grad", "profiled_rates", "clocks",
-              "init_s"):
+              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "lanes_vs_sim", "memory", "ps_gain", "grad",
+              "profiled_rates", "clocks", "init_s"):
         line[k] = head[k]
     if dist:
         line["nccl_ranks"] = dist.get_world_size()
@@ -600,7 +609,8 @@ def main():
             r = run_workload(a, name, GPU_BUDGET_GIB[name], a.steps, a.warmup, rank, world, local, None,
                              headline=False)
             sec[name] = {k: r[k] for k in ("value", "ms_per_step", "e2e", "roofline", "mfu_model", "bound_by",
-                                           "lane_busy_ms_per_step", "plan", "offload", "ps_gain", "grad", "clocks")}
+                                           "lane_busy_ms_per_step", "lanes_vs_sim", "memory", "plan", "offload",
+                                           "ps_gain", "grad", "clocks")}
             sec[name]["workload"] = workload_config(argparse.Namespace(config=name, strategy="",
                                                                        gpu_mem_gib=GPU_BUDGET_GIB[name]),
                                                     CONFIGS[name], 1)["workload"]

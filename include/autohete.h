@@ -156,10 +156,12 @@ int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int32_
                            int32_t heads, int32_t head_dim, void* stream);
 
 /* Flash attention backward: from qkv, O, dO [B, s, h] and lse2 -> dqkv [B, s, 3h] bf16 (dQ, dK,
- * dV of every head; P recomputed). Scratch (B*heads*s*(s*2 + 4) bytes) is stream-allocated. */
+ * dV of every head; P recomputed). workspace: caller-owned device scratch of at least
+ * ah_attention_flash_bwd_workspace(batch, seq_len, heads) bytes (16-byte aligned). */
+size_t ah_attention_flash_bwd_workspace(int32_t batch, int32_t seq_len, int32_t heads);
 int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2,
                            uint16_t* dqkv, int32_t batch, int32_t seq_len, int32_t heads, int32_t head_dim,
-                           void* stream);
+                           void* workspace, size_t workspace_bytes, void* stream);
 
 /* LayerNorm of the block step (part of OpKind::Forward / Backward / Recompute; no reference
  * kernel — the reference times the whole block as t_fp / t_bp, workload.cpp:55-67).
@@ -169,9 +171,13 @@ int ah_layernorm_fwd(const uint16_t* x, const uint16_t* gamma, const uint16_t* b
 /* dx = LN'(dy) (+ dres if non-null); dgamma_dbeta [2h] = [sum dy*xhat | sum dy] (bf16).
  * Optional fused bias gradients (h % 256 == 0): dres_colsum [h] = column sums of dres,
  * dx_colsum [h] = column sums of bf16(dx). Deterministic (fixed-order reductions). */
+/* workspace: caller-owned device scratch of ah_layernorm_bwd_workspace(rows, h) bytes (the
+ * fixed-order column-reduction partials). */
+size_t ah_layernorm_bwd_workspace(int32_t rows, int32_t h);
 int ah_layernorm_bwd(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd,
                      const uint16_t* gamma, const uint16_t* dres, uint16_t* dx, uint16_t* dgamma_dbeta,
-                     uint16_t* dres_colsum, uint16_t* dx_colsum, int32_t rows, int32_t h, void* stream);
+                     uint16_t* dres_colsum, uint16_t* dx_colsum, int32_t rows, int32_t h, void* workspace,
+                     size_t workspace_bytes, void* stream);
 
 /* ---------------------------------------------------------------------------------------
  * Training executor: one GPT iteration = hetsim::build_iteration_ops(profile, strategy, k)
@@ -222,6 +228,25 @@ int ah_dp_loopback_create(int32_t nranks, void** comm);
 int ah_dp_loopback_destroy(void* comm);
 int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard);
 
+/* ---------------------------------------------------------------------------------------
+ * Data-parallel collectives of north_star (d) as standalone entry points (the executor issues
+ * the same calls internally). The reference has no multi-GPU path; these realise
+ * the per-block exchange around its ops: the all-gather before a block's first use in F / R / B
+ * (bf16 params, after ParamPrefetch / materialisation, simulator.hpp:16-32) and the
+ * reduce-scatter after its Backward (bf16 grads, before GradOffload / GpuOptim). NCCL over
+ * NVLink / NVSwitch; one communicator per rank (device = the caller's current device).
+ * --------------------------------------------------------------------------------------- */
+/* nccl_id: 128 bytes from ah_dp_unique_id on rank 0, broadcast by the caller. Setup call. */
+int ah_nccl_comm_create(const uint8_t* nccl_id, int32_t nranks, int32_t rank, void** comm);
+int ah_nccl_comm_destroy(void* comm);
+/* bf16 SUM over ranks of send [nranks * count] -> recv [count] = this rank's shard (the grads of
+ * elements [rank*count, (rank+1)*count)); in place when recv == send + rank * count. */
+int ah_nccl_reduce_scatter_bf16(const uint16_t* send, uint16_t* recv, size_t count, void* comm, void* stream);
+/* send [count] (this rank's shard) -> recv [nranks * count]; in place when send == recv + rank * count. */
+int ah_nccl_all_gather_bf16(const uint16_t* send, uint16_t* recv, size_t count, void* comm, void* stream);
+/* In-place SUM all-reduce of the replicated groups' grads; dtype 0 = fp32, 1 = bf16. */
+int ah_nccl_all_reduce(void* buf, size_t count, int32_t dtype, void* comm, void* stream);
+
 typedef struct ah_trainer_stats {
     int32_t c_hat, p_hat, o_hat;
     double activation_coef;       /* real bytes of a block's activations / (2*b*s*h) */
@@ -255,6 +280,9 @@ typedef struct ah_trainer_stats {
     double grad_norm;
     int64_t nonfinite_grads;
     int32_t skipped_updates;
+    /* the reference scheduler's per-lane busy time of one steady-state iteration (compute, h2d,
+     * d2h, cpu; ms) for the plan and order in use — the simulated counterpart of lane_busy_ms */
+    double sim_lane_busy_ms[4];
 } ah_trainer_stats;
 
 int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);
@@ -282,6 +310,11 @@ int64_t ah_trainer_master_size(void* trainer, int32_t block);
 int ah_trainer_save(void* trainer, const char* path);
 int ah_trainer_load(void* trainer, const char* path);
 int ah_trainer_trace(void* trainer, char* buf, size_t cap); /* Chrome trace JSON, measured */
+/* Measured GPU-memory timeline of the last drained iterations in the reference's CSV schema
+ * ("time_us,gpu_bytes", simulator.cpp:615-622): persistent allocations + the executor's
+ * transient buffers taken at each op's start / returned at its end (CUDA-event times).
+ * Returns the bytes needed (incl. NUL) like ah_trainer_trace; *peak_bytes (nullable) = max. */
+int ah_trainer_memory_csv(void* trainer, char* buf, size_t cap, int64_t* peak_bytes);
 /* Device-timed region on the executor's compute stream: stop=0 drains then records the
  * start event; stop=1 drains all lanes, records the stop event and returns elapsed ms. */
 int ah_trainer_timer(void* trainer, int32_t stop, float* ms);

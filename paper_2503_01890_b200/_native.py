@@ -150,7 +150,7 @@ class TrainerStats(C.Structure):
         ("copy_blocked_ms", C.c_double), ("upstream_blocked_ms", C.c_double), ("cpu_busy_ms", C.c_double),
         ("window_ms", C.c_double), ("sim_steady_fifo_s", C.c_double), ("sim_steady_ps_s", C.c_double),
         ("priority_sched", C.c_int32), ("grad_norm", C.c_double), ("nonfinite_grads", C.c_int64),
-        ("skipped_updates", C.c_int32),
+        ("skipped_updates", C.c_int32), ("sim_lane_busy_ms", C.c_double * 4),
     ]
 
 
@@ -182,6 +182,7 @@ class HostProfile(C.Structure):
 
 _EXTRA_SIGS.update({
     "ah_trainer_set_schedule": ([C.c_void_p, C.c_int32], C.c_int),
+    "ah_trainer_memory_csv": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)], C.c_int),
     "ah_profile_host": ([C.c_size_t, C.c_int32, C.POINTER(HostProfile)], C.c_int),
     "ah_trainer_timer": ([C.c_void_p, C.c_int32, C.POINTER(C.c_float)], C.c_int),
     "ah_profile_block": ([C.POINTER(TrainerConfig), C.POINTER(HwProfile)], C.c_int),
@@ -195,6 +196,15 @@ _EXTRA_SIGS.update({
     "ah_dp_loopback_destroy": ([C.c_void_p], C.c_int),
     "ah_dp_shard": ([C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                      C.POINTER(C.c_int64)], C.c_int),
+})
+
+
+_EXTRA_SIGS.update({
+    "ah_nccl_comm_create": ([C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
+    "ah_nccl_comm_destroy": ([C.c_void_p], C.c_int),
+    "ah_nccl_reduce_scatter_bf16": ([C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p], C.c_int),
+    "ah_nccl_all_gather_bf16": ([C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p], C.c_int),
+    "ah_nccl_all_reduce": ([C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p, C.c_void_p], C.c_int),
 })
 
 

@@ -3,6 +3,7 @@
 #include "../kernels/gemm.h"
 #include "../kernels/gpt_kernels.h"
 #include <cmath>
+#include <cstdint>
 #include "capi_util.h"
 
 extern "C" int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
@@ -25,21 +26,28 @@ extern "C" int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* l
                            "ah_attention_flash_fwd");
 }
 
+// scratch: D = rowsum(dO * O) [B*heads*s] fp32, then dS^T [B*heads, s, s] bf16 (16-byte aligned)
+extern "C" size_t ah_attention_flash_bwd_workspace(int32_t batch, int32_t seq_len, int32_t heads) {
+    const size_t rows = (size_t)batch * heads * seq_len;
+    return (rows * 4 + 255) / 256 * 256 + rows * (size_t)seq_len * 2;
+}
+
 extern "C" int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2,
                                       uint16_t* dqkv, int32_t batch, int32_t seq_len, int32_t heads, int32_t head_dim,
-                                      void* stream) {
-    if (!qkv || !O || !dO || !lse2 || !dqkv) return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: null argument");
+                                      void* workspace, size_t workspace_bytes, void* stream) {
+    if (!qkv || !O || !dO || !lse2 || !dqkv || !workspace)
+        return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: null argument");
     if (!ah::gpt::flash_supported(head_dim, seq_len))
         return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: needs head_dim 128 and seq_len % 128 == 0");
+    if (workspace_bytes < ah_attention_flash_bwd_workspace(batch, seq_len, heads) ||
+        (reinterpret_cast<uintptr_t>(workspace) & 15u))
+        return ah::set_error(AH_ERR_INVALID, "ah_attention_flash_bwd: workspace too small or not 16-byte aligned");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     const long long s = seq_len, h = (long long)heads * head_dim, rows = (long long)batch * heads * s;
     const float scale = 1.0f / std::sqrt((float)head_dim);
-    float* D = nullptr;
-    uint16_t* dS = nullptr;
-    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&D), rows * 4, st);
-    if (e == cudaSuccess) e = cudaMallocAsync(reinterpret_cast<void**>(&dS), rows * s * 2, st);
-    if (e == cudaSuccess)
-        e = ah::gpt::flash_bwd(qkv, O, dO, lse2, D, dS, dqkv, batch, seq_len, heads, head_dim, scale, st);
+    float* D = static_cast<float*>(workspace);
+    uint16_t* dS = reinterpret_cast<uint16_t*>(static_cast<char*>(workspace) + ((size_t)rows * 4 + 255) / 256 * 256);
+    cudaError_t e = ah::gpt::flash_bwd(qkv, O, dO, lse2, D, dS, dqkv, batch, seq_len, heads, head_dim, scale, st);
     if (e == cudaSuccess) {  // dQ = dS K * scale (causal: K range up to the query tile)
         ah::gemm::GemmArgs g;
         g.batch1 = heads;
@@ -53,7 +61,5 @@ extern "C" int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, co
         g.causal = ah::gemm::kCausalKUptoM;
         e = ah::gemm::run(g, st);
     }
-    if (D) cudaFreeAsync(D, st);
-    if (dS) cudaFreeAsync(dS, st);
     return ah::cuda_status(e, "ah_attention_flash_bwd");
 }

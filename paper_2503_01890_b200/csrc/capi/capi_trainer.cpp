@@ -119,6 +119,14 @@ int ah_trainer_trace(void* tr, char* buf, size_t cap) {
     return copy_out(s, buf, cap);
 }
 
+int ah_trainer_memory_csv(void* tr, char* buf, size_t cap, int64_t* peak_bytes) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    std::string s;
+    const int rc = guarded([&] { s = T(tr)->memory_csv(peak_bytes); });
+    if (rc != AH_OK) return rc;
+    return copy_out(s, buf, cap);
+}
+
 }  // extern "C"
 
 namespace ah {
@@ -170,6 +178,50 @@ int ah_dp_loopback_create(int32_t nranks, void** comm) {
 int ah_dp_loopback_destroy(void* comm) {
     delete static_cast<ah::LoopbackComm*>(comm);
     return AH_OK;
+}
+
+namespace {
+int nccl_status(ncclResult_t r, const char* where) {
+    if (r == ncclSuccess) return AH_OK;
+    return ah::set_error(AH_ERR_NCCL, std::string(where) + ": " + ncclGetErrorString(r));
+}
+ncclComm_t C_(void* c) { return static_cast<ncclComm_t>(c); }
+}  // namespace
+
+int ah_nccl_comm_create(const uint8_t* nccl_id, int32_t nranks, int32_t rank, void** comm) {
+    if (!nccl_id || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+        return ah::set_error(AH_ERR_INVALID, "ah_nccl_comm_create: bad argument");
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof(id));
+    ncclComm_t c = nullptr;
+    const int rc = nccl_status(ncclCommInitRank(&c, nranks, id, rank), "ncclCommInitRank");
+    if (rc == AH_OK) *comm = c;
+    return rc;
+}
+
+int ah_nccl_comm_destroy(void* comm) {
+    if (!comm) return ah::set_error(AH_ERR_INVALID, "ah_nccl_comm_destroy: null comm");
+    return nccl_status(ncclCommDestroy(C_(comm)), "ncclCommDestroy");
+}
+
+int ah_nccl_reduce_scatter_bf16(const uint16_t* send, uint16_t* recv, size_t count, void* comm, void* stream) {
+    if (!send || !recv || !comm) return ah::set_error(AH_ERR_INVALID, "ah_nccl_reduce_scatter_bf16: null argument");
+    return nccl_status(ncclReduceScatter(send, recv, count, ncclBfloat16, ncclSum, C_(comm),
+                                         static_cast<cudaStream_t>(stream)),
+                       "ncclReduceScatter");
+}
+
+int ah_nccl_all_gather_bf16(const uint16_t* send, uint16_t* recv, size_t count, void* comm, void* stream) {
+    if (!send || !recv || !comm) return ah::set_error(AH_ERR_INVALID, "ah_nccl_all_gather_bf16: null argument");
+    return nccl_status(ncclAllGather(send, recv, count, ncclBfloat16, C_(comm), static_cast<cudaStream_t>(stream)),
+                       "ncclAllGather");
+}
+
+int ah_nccl_all_reduce(void* buf, size_t count, int32_t dtype, void* comm, void* stream) {
+    if (!buf || !comm || (dtype != 0 && dtype != 1)) return ah::set_error(AH_ERR_INVALID, "ah_nccl_all_reduce: bad argument");
+    return nccl_status(ncclAllReduce(buf, buf, count, dtype ? ncclBfloat16 : ncclFloat32, ncclSum, C_(comm),
+                                     static_cast<cudaStream_t>(stream)),
+                       "ncclAllReduce");
 }
 
 int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard) {

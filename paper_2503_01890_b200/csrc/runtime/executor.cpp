@@ -249,9 +249,11 @@ void Trainer::plan(const ah_trainer_config& cfg) {
 void Trainer::compile_order() {
     for (auto& it : order_)
         for (auto& lane : it) lane.clear();
+    for (double& x : sim_lane_ms_) x = 0.0;
     for (const hetsim::CompletedOp& op : sim_.trace) {
         if (op.iter > 2) continue;
         order_[op.iter - 1][lane_of(op.kind)].push_back({(int)op.kind, op.block, op.backward_copy});
+        if (op.iter == 2) sim_lane_ms_[lane_of(op.kind)] += (op.end - op.start) * 1e3;
     }
 }
 
@@ -519,7 +521,7 @@ void Trainer::lane_main(int lane) {
                 }
                 cv_.notify_all();
                 if (lane == kCompute) {
-                    prefetch_weights(*it, idx);  // the next op's weights, overlapping this op
+                    prefetch_weights(*it, idx, op);  // the next op's weights, overlapping this op
                     run_compute(*it, op);
                 }
                 else if (lane == kH2D)
@@ -653,6 +655,7 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
     const size_t off = shard_ * (size_t)dp_rank_;
     auto materialize = [&]() {  // bf16 weights from the on-GPU fp32 master (footnote 2)
         check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, st), "alloc wbuf");
+        op.alloc_b += (int64_t)full_len() * 2;
         if (dp_) {  // own shard, then all-gather the others over NVLink (side stream)
             check(launch_cast_f32_bf16(b.master, b.wbuf + off, shard_, st), "cast");
             side_after_compute();
@@ -672,14 +675,19 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
         compute_after_side();
         b.needs_gather = false;
     }
-    auto alloc_acts = [&]() { check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts"); };
+    auto alloc_acts = [&]() {
+        check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts");
+        op.alloc_b += (int64_t)BlockActs::bytes(d_);
+    };
     auto free_acts = [&]() {
         check(cudaFreeAsync(b.acts, st), "free acts");
         b.acts = nullptr;
+        op.free_b += (int64_t)BlockActs::bytes(d_);
     };
     auto free_wbuf = [&]() {
         check(cudaFreeAsync(b.wbuf, st), "free wbuf");
         b.wbuf = nullptr;
+        op.free_b += (int64_t)full_len() * 2;
     };
     switch (op.kind) {
         case OpKind::Forward: {
@@ -742,6 +750,7 @@ void Trainer::run_h2d(Iter& it, RtOp& op) {
     const size_t n = dp_ ? shard_ : mp;  // DP: only this rank's shard crosses the host link
     uint16_t* dst = nullptr;
     check(cudaMallocAsync((void**)&dst, full_len() * 2, s_h2d_), "alloc prefetch");
+    op.alloc_b += (int64_t)full_len() * 2;
     uint16_t* mine = dp_ ? dst + shard_ * (size_t)dp_rank_ : dst;
     if (b.o)
         check(cudaMemcpyAsync(mine, b.host_bf16, n * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
@@ -763,6 +772,7 @@ void Trainer::run_d2h(Iter& it, RtOp& op) {
           "offload stats");
     check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
     b.wbuf = nullptr;
+    op.free_b += (int64_t)full_len() * 2;
 }
 
 void Trainer::run_cpu(Iter& it, RtOp& op) {
@@ -825,7 +835,7 @@ void Trainer::compute_after_side() {
 // (F, R or B of a non-O, non-P block whose buffer is not live), do it now on the side stream —
 // cast from the fp32 master (+ DP all-gather) — so it overlaps op idx instead of preceding the
 // next op on the compute stream. Only the compute lane thread touches these blocks' buffers.
-void Trainer::prefetch_weights(const Iter& it, size_t idx) {
+void Trainer::prefetch_weights(const Iter& it, size_t idx, RtOp& cur) {
     if (!prefetch_mat_) return;
     const std::vector<OpKey>& order = it.lane_order[kCompute];
     if (idx + 1 >= order.size()) return;
@@ -838,6 +848,7 @@ void Trainer::prefetch_weights(const Iter& it, size_t idx) {
     if (b.o || b.p || b.wbuf || b.mat_pending) return;
     side_after_compute();  // the master is final: every compute op enqueued so far precedes the cast
     check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, s_side_), "alloc wbuf");
+    cur.alloc_b += (int64_t)full_len() * 2;  // lives from the current op on
     if (dp_) {
         check(launch_cast_f32_bf16(b.master, b.wbuf + shard_ * (size_t)dp_rank_, shard_, s_side_), "cast");
         dp_gather(b.wbuf, s_side_);
@@ -941,6 +952,7 @@ void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_devi
     for (Iter* old : retired_) {
         for (auto& kv : old->ops) {
             RtOp& o = kv.second;
+            retired_bytes_ += o.alloc_b - o.free_b;
             if (o.lane != kCpu && o.host_ms >= 0) {  // account GPU lane time before the events go
                 float ms = 0.f;
                 if (cudaEventSynchronize(o.t1) == cudaSuccess && cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
@@ -1067,6 +1079,7 @@ void Trainer::stats(ah_trainer_stats* s) {
     s->grad_norm = grad_norm_;
     s->nonfinite_grads = nonfinite_;
     s->skipped_updates = skipped_;
+    for (int l = 0; l < 4; ++l) s->sim_lane_busy_ms[l] = sim_lane_ms_[l];
 }
 
 std::string Trainer::trace_json() {
@@ -1092,6 +1105,40 @@ std::string Trainer::trace_json() {
         return x.start < y.start;
     });
     hetsim::write_chrome_trace(out, ops);
+    return out.str();
+}
+
+std::string Trainer::memory_csv(int64_t* peak_bytes) {
+    std::lock_guard<std::mutex> lk(mu_);
+    std::vector<std::pair<double, int64_t>> ev;  // (time s, delta bytes)
+    cudaEvent_t origin = nullptr;
+    float first = 0.f;
+    for (Iter* it : iters_)
+        for (auto& kv : it->ops) {
+            RtOp& o = kv.second;
+            if (o.lane == kCpu || (!o.alloc_b && !o.free_b)) continue;
+            if (!origin) origin = o.t0;
+            float a = 0.f, b = 0.f;
+            if (cudaEventElapsedTime(&a, origin, o.t0) != cudaSuccess) continue;
+            if (cudaEventElapsedTime(&b, origin, o.t1) != cudaSuccess) continue;
+            first = std::min(first, a);
+            if (o.alloc_b) ev.push_back({a / 1e3, o.alloc_b});
+            if (o.free_b) ev.push_back({b / 1e3, -o.free_b});
+        }
+    std::sort(ev.begin(), ev.end(), [](const auto& x, const auto& y) {
+        return x.first != y.first ? x.first < y.first : x.second < y.second;  // frees first on ties
+    });
+    std::vector<std::pair<double, int64_t>> tl;
+    int64_t cur = (int64_t)static_bytes_ + retired_bytes_, peak = cur;
+    tl.push_back({0.0, cur});
+    for (const auto& e : ev) {
+        cur += e.second;
+        peak = std::max(peak, cur);
+        tl.push_back({e.first - first / 1e3, cur});
+    }
+    if (peak_bytes) *peak_bytes = peak;
+    std::ostringstream out;
+    hetsim::write_memory_csv(out, tl);
     return out.str();
 }
 

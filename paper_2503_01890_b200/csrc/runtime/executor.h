@@ -60,6 +60,11 @@ public:
     size_t master_size(int block) const;
     // Chrome trace of the last drained iterations in the reference schema (simulator.cpp:598).
     std::string trace_json();
+    // Measured GPU-memory timeline of the drained window in the reference CSV schema
+    // (write_memory_csv, simulator.cpp:615-622): persistent allocations + the executor's
+    // stream-ordered transient buffers, taken at each op's start and returned at its end
+    // (CUDA-event times, µs from the window's first op).
+    std::string memory_csv(int64_t* peak_bytes = nullptr);
     // drain + record start (stop=false) / drain + record stop and return elapsed ms (stop=true)
     float timer(bool stop);
     // Optimizer-state checkpoint (fp32 master, m, v of this rank's part of every block + the
@@ -107,6 +112,7 @@ private:
         int state = 0;  // 0 pending, 1 started (start_ev recorded), 2 issued (done_ev recorded), 3 done (host)
         double host_ms = 0.0;
         bool done_on_side = false;  // DP backward: done_ev follows the gradient reduce-scatter on s_side_
+        int64_t alloc_b = 0, free_b = 0;  // stream-ordered pool bytes taken at its start / returned at its end
     };
     struct Iter {
         long long k = 0;
@@ -138,7 +144,7 @@ private:
     void wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side = false);
     // Side stream: materialisation of the next compute op's weights (overlapping the current
     // op) and every NCCL collective, issued by the compute lane thread in op order.
-    void prefetch_weights(const Iter& it, size_t idx);
+    void prefetch_weights(const Iter& it, size_t idx, RtOp& cur);
     void side_after_compute();
     void compute_after_side();
     RtOp* find(long long iter, const OpKey& key);
@@ -160,6 +166,7 @@ private:
     hetsim::dp::DpSpec dp_spec_;
     hetsim::SimResult sim_;
     double sim_steady_[2] = {0.0, 0.0};  // reference scheduler steady state: [0] FIFO, [1] PS
+    double sim_lane_ms_[4] = {0, 0, 0, 0};  // simulated busy time per lane, steady iteration
     void compile_order();                // order_ from sim_
     bool ps_ = true;
     ah_adam_hparams adam_{};
@@ -225,6 +232,7 @@ private:
     void grad_stats_pass(int slot, const uint16_t* g, size_t n, cudaStream_t st);
     void collect_grad_stats();
     void account_window();
+    int64_t retired_bytes_ = 0;  // net transient bytes of ops in iterations already retired
 };
 
 }  // namespace ah

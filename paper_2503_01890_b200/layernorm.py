@@ -43,10 +43,15 @@ def layernorm_bwd(dy, x, mean, rstd, gamma, dres=None, bias_sums=False):
     dgdb = torch.empty(2 * h, dtype=torch.bfloat16, device=x.device)
     cr = torch.empty(h, dtype=torch.bfloat16, device=x.device) if bias_sums and dres is not None else None
     cx = torch.empty(h, dtype=torch.bfloat16, device=x.device) if bias_sums else None
-    fn = N.lib().ah_layernorm_bwd
-    fn.argtypes = [_P] * 10 + [C.c_int32, C.c_int32, _P]
+    L = N.lib()
+    L.ah_layernorm_bwd_workspace.argtypes = [C.c_int32, C.c_int32]
+    L.ah_layernorm_bwd_workspace.restype = C.c_size_t
+    nbytes = L.ah_layernorm_bwd_workspace(rows, h)
+    ws = torch.empty(max(nbytes, 16), dtype=torch.uint8, device=x.device)
+    fn = L.ah_layernorm_bwd
+    fn.argtypes = [_P] * 10 + [C.c_int32, C.c_int32, _P, C.c_size_t, _P]
     fn.restype = C.c_int
     N.check(fn(dy.data_ptr(), x.data_ptr(), mean.data_ptr(), rstd.data_ptr(), gamma.data_ptr(), _ptr(dres),
-               dx.data_ptr(), dgdb.data_ptr(), _ptr(cr), _ptr(cx), rows, h,
+               dx.data_ptr(), dgdb.data_ptr(), _ptr(cr), _ptr(cx), rows, h, ws.data_ptr(), nbytes,
                torch.cuda.current_stream().cuda_stream), "ah_layernorm_bwd")
     return dx, dgdb, cr, cx

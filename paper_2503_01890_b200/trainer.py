@@ -141,6 +141,7 @@ class Trainer:
         out = {f: getattr(s, f) for f, _ in s._fields_}
         out["lane_busy_ms"] = list(s.lane_busy_ms)
         out["lane_ops"] = list(s.lane_ops)
+        out["sim_lane_busy_ms"] = list(s.sim_lane_busy_ms)
         return out
 
     def reset_stats(self) -> None:
@@ -169,6 +170,17 @@ class Trainer:
     def load(self, path: str) -> None:
         """Resume from save() into a fresh trainer (any plan, same model / dp layout)."""
         N.check(N.lib().ah_trainer_load(self._h, path.encode()), "ah_trainer_load")
+
+    def memory_csv(self) -> tuple[str, int]:
+        """Measured GPU-memory timeline ("time_us,gpu_bytes", the reference's CSV schema) of the
+        last drained iterations, and its peak in bytes."""
+        peak = C.c_int64()
+        n = N.lib().ah_trainer_memory_csv(self._h, None, 0, C.byref(peak))
+        if n < 0:
+            N.check(n, "ah_trainer_memory_csv")
+        buf = C.create_string_buffer(n + 4096)
+        N.check(min(0, N.lib().ah_trainer_memory_csv(self._h, buf, len(buf), C.byref(peak))), "ah_trainer_memory_csv")
+        return buf.value.decode(), peak.value
 
     def timer(self, stop: bool) -> float:
         ms = C.c_float()

@@ -55,7 +55,7 @@ def loss_and_grads(blocks, wte, wpe, lnf, tokens, targets, nh, V):
     wpe_ = wpe.clone().requires_grad_(True)
     lnf_ = lnf.clone().requires_grad_(True)
     B, s = tokens.shape
-    x = wte_[tokens] + wpe_[torch.arange(s)]
+    x = wte_[tokens] + wpe_[torch.arange(s, device=tokens.device)]
     for p in params:
         x = block_fwd(x, unflatten(p, h), nh)
     x = F.layer_norm(x, (h,), lnf_[:h], lnf_[h:], eps=1e-5)

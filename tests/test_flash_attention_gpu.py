@@ -26,7 +26,9 @@ def rel(a, b):
     return float((a.detach().float() - b.detach().float()).norm() / b.detach().float().norm())
 
 
-@pytest.mark.parametrize("B,s,nh,amp", [(1, 128, 1, 0.5), (2, 256, 2, 0.5), (2, 1024, 4, 0.5), (1, 512, 2, 4.0)])
+@pytest.mark.parametrize("B,s,nh,amp", [(1, 128, 1, 0.5), (2, 256, 2, 0.5), (2, 1024, 4, 0.5), (1, 512, 2, 4.0),
+                                        # the BASELINE block shapes: 1.3B (b=8, 16 heads), 10B (48), 20B (64)
+                                        (8, 1024, 16, 0.5), (1, 1024, 48, 0.5), (1, 1024, 64, 1.0)])
 def test_flash_forward_and_backward(cuda_device, native, B, s, nh, amp):
     """amp 4.0 gives large score ranges, exercising the lazy O / l rescale."""
     from paper_2503_01890_b200.attention import flash_bwd, flash_fwd

@@ -236,3 +236,25 @@ def test_set_schedule_switches_to_fifo(cuda_device, native):
     assert loss == base_loss[-1]
     for a, b in zip(state, base_state):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_measured_memory_timeline(cuda_device, native):
+    """The executor's measured memory timeline is in the reference's CSV schema (time_us,
+    gpu_bytes; simulator.cpp:615-622), starts at the persistent allocations, is time-ordered, and
+    stays within the scheduler's simulated peak for the same plan."""
+    from paper_2503_01890_b200.trainer import PlanConfig
+    tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=3, fine_tune=False, gpu_mem_budget=1 << 40))
+    for k in range(3):
+        tr.submit(*batch(k))
+    tr.drain()
+    csv, peak = tr.memory_csv()
+    st = tr.stats()
+    tr.close()
+    lines = csv.strip().splitlines()
+    assert lines[0] == "time_us,gpu_bytes" and len(lines) > 10
+    rows = [tuple(int(x) for x in l.split(",")) for l in lines[1:]]
+    assert all(b[0] >= a[0] for a, b in zip(rows, rows[1:]))
+    assert rows[0][1] >= st["static_bytes"] and peak == max(r[1] for r in rows)
+    assert peak <= 1.05 * st["simulated_peak_bytes"], (peak, st["simulated_peak_bytes"])
+    sim = st["sim_lane_busy_ms"]
+    assert sim[0] > 0 and sim[1] > 0 and sim[2] > 0 and sim[3] > 0
