@@ -324,13 +324,22 @@ int ah_trainer_timer(void* trainer, int32_t stop, float* ms);
  * returns the HardwareSpec rates the planner consumes. Reference counterpart: the analytic
  * estimate_block_times (proj/core/src/workload.cpp:55-73), which this replaces.
  * --------------------------------------------------------------------------------------- */
+/* GPU times are taken after >= 1 s of back-to-back block forward + backward (the power-capped
+ * sustained clock a training step runs at, not the idle-GPU boost clock). The reference model
+ * has per-block times only (workload.cpp:55-73), so the per-iteration work outside the blocks —
+ * embedding forward / backward, final LayerNorm, LM-head GEMMs, cross-entropy, the embedding
+ * group's AdamW — is measured on the real shapes and folded into every block's time as a 1/L
+ * share: L * t_fwd_s + L * t_bwd_s is the whole compute-lane iteration. */
 typedef struct ah_hw_profile {
-    double t_fwd_s, t_bwd_s;  /* one block, measured */
+    double t_fwd_s, t_bwd_s;  /* per block incl. the 1/L share of non-block work (what the planner uses) */
     double gpu_flops;         /* (2*m_p*b*s + 4*b*s^2*h) / t_fwd_s, workload.cpp:63 */
     double bwd_fwd_ratio;     /* t_bwd_s / t_fwd_s -> ModelSpec::bwd_fwd_ratio */
     double h2d_bw, d2h_bw;    /* pinned 2*m_p-byte copies, B/s */
     double gpu_adam_rate;     /* params/s, fused sm_100a AdamW */
-    double cpu_adam_rate;     /* params/s, host AdamW with cfg->cpu_threads */
+    double cpu_adam_rate;     /* params/s, host AdamW with cfg->cpu_threads over >= 2 GB of distinct
+                               * block states (DRAM-resident, as in the step), median of 3 passes */
+    double t_block_fwd_s, t_block_bwd_s;        /* the block alone (sustained clock) */
+    double t_nonblock_fwd_s, t_nonblock_bwd_s;  /* per iteration, outside the blocks */
 } ah_hw_profile;
 int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out);
 

@@ -172,7 +172,9 @@ _EXTRA_SIGS.update({
 class HwProfile(C.Structure):
     _fields_ = [("t_fwd_s", C.c_double), ("t_bwd_s", C.c_double), ("gpu_flops", C.c_double),
                 ("bwd_fwd_ratio", C.c_double), ("h2d_bw", C.c_double), ("d2h_bw", C.c_double),
-                ("gpu_adam_rate", C.c_double), ("cpu_adam_rate", C.c_double)]
+                ("gpu_adam_rate", C.c_double), ("cpu_adam_rate", C.c_double),
+                ("t_block_fwd_s", C.c_double), ("t_block_bwd_s", C.c_double),
+                ("t_nonblock_fwd_s", C.c_double), ("t_nonblock_bwd_s", C.c_double)]
 
 
 class HostProfile(C.Structure):

@@ -258,3 +258,27 @@ def test_measured_memory_timeline(cuda_device, native):
     assert peak <= 1.05 * st["simulated_peak_bytes"], (peak, st["simulated_peak_bytes"])
     sim = st["sim_lane_busy_ms"]
     assert sim[0] > 0 and sim[1] > 0 and sim[2] > 0 and sim[3] > 0
+
+
+def test_profile_block(cuda_device, native):
+    """Runtime profiler (paper §3.1): rates are positive and self-consistent — the planner's
+    per-block times include a 1/L share of the measured non-block work, gpu_flops reproduces
+    t_fwd through the reference's t_fp formula (workload.cpp:63), and the CPU AdamW rate is
+    the DRAM-resident one (below the host stream roofline)."""
+    from paper_2503_01890_b200.trainer import ModelConfig, profile_hardware, profile_host
+    m = ModelConfig(**MODEL)
+    p = profile_hardware(m, cpu_threads=4)
+    for k in ("t_fwd_s", "t_bwd_s", "gpu_flops", "h2d_bw", "d2h_bw", "gpu_adam_rate", "cpu_adam_rate",
+              "t_block_fwd_s", "t_block_bwd_s", "t_nonblock_fwd_s", "t_nonblock_bwd_s"):
+        assert p[k] > 0 and np.isfinite(p[k]), k
+    L, h, s, B = MODEL["num_blocks"], MODEL["hidden"], MODEL["seq_len"], MODEL["batch"]
+    assert abs(p["t_fwd_s"] - (p["t_block_fwd_s"] + p["t_nonblock_fwd_s"] / L)) < 1e-12
+    assert abs(p["t_bwd_s"] - (p["t_block_bwd_s"] + p["t_nonblock_bwd_s"] / L)) < 1e-12
+    mp = 12 * h * h + 13 * h
+    flops = 2.0 * mp * B * s + 4.0 * B * s * s * h
+    assert abs(flops / p["gpu_flops"] - p["t_fwd_s"]) < 1e-9 * p["t_fwd_s"] + 1e-15
+    assert abs(p["bwd_fwd_ratio"] - p["t_bwd_s"] / p["t_fwd_s"]) < 1e-9
+    assert 5e9 < p["h2d_bw"] < 1e12 and 5e9 < p["d2h_bw"] < 1e12
+    host = profile_host(20_000_000, 4)
+    assert host["stream_gbps"] > 0 and host["adam_gbps"] > 0
+    assert p["cpu_adam_rate"] * 28 / 1e9 < 1.5 * host["stream_gbps"]
