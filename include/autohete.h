@@ -143,14 +143,9 @@ typedef struct ah_gemm_desc {
 
 int ah_gemm_bf16(const ah_gemm_desc* desc, void* stream);
 
-/* Fused causal attention forward of one block (part of OpKind::Forward / Recompute; the
- * reference's 4*b*s^2*h attention term of t_fp, workload.cpp:63): qkv [B, s, 3h] bf16 ->
- * O [B, s, h] bf16 and the normalised probabilities P [B, heads, s, s] bf16 (saved for the
- * backward; zero above the diagonal within each 128-row tile). head_dim must be 128. */
-int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
-                     int32_t heads, int32_t head_dim, void* stream);
-
-/* Flash attention forward (the executor's default): qkv [B, s, 3h] bf16 -> O [B, s, h] bf16 and
+/* Fused causal attention of one block (part of OpKind::Forward / Recompute / Backward; the
+ * reference's 4*b*s^2*h attention term of t_fp, workload.cpp:63). head_dim must be 128.
+ * Flash attention forward: qkv [B, s, 3h] bf16 -> O [B, s, h] bf16 and
  * lse2 [B, heads, s] fp32, the per-row log2-domain log-sum-exp of the scaled scores. */
 int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int32_t batch, int32_t seq_len,
                            int32_t heads, int32_t head_dim, void* stream);

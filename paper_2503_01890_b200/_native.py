@@ -225,5 +225,4 @@ def dp_shard(n: int, rank: int, size: int) -> tuple[int, int, int]:
 _EXTRA_SIGS.update({
     "ah_trainer_save": ([C.c_void_p, C.c_char_p], C.c_int),
     "ah_trainer_load": ([C.c_void_p, C.c_char_p], C.c_int),
-    "ah_attention_fwd": ([C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_void_p], C.c_int),
 })

@@ -1,20 +1,11 @@
-// extern "C" test / instrumentation entry for the fused attention forward.
+// extern "C" entries of the flash attention kernels (tests / profiling; the executor calls them
+// from C++ inside block_forward / block_backward).
 #include "autohete.h"
 #include "../kernels/gemm.h"
 #include "../kernels/gpt_kernels.h"
 #include <cmath>
 #include <cstdint>
 #include "capi_util.h"
-
-extern "C" int ah_attention_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int32_t batch, int32_t seq_len,
-                                int32_t heads, int32_t head_dim, void* stream) {
-    if (!qkv || !P || !O) return ah::set_error(AH_ERR_INVALID, "ah_attention_fwd: null argument");
-    if (!ah::gpt::attn_fwd_supported(head_dim, seq_len))
-        return ah::set_error(AH_ERR_INVALID, "ah_attention_fwd: needs head_dim 128 and seq_len % 128 == 0");
-    return ah::cuda_status(ah::gpt::attn_fwd(qkv, P, O, batch, seq_len, heads, head_dim,
-                                             1.0f / __builtin_sqrtf((float)head_dim), static_cast<cudaStream_t>(stream)),
-                           "ah_attention_fwd");
-}
 
 extern "C" int ah_attention_flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int32_t batch, int32_t seq_len,
                                       int32_t heads, int32_t head_dim, void* stream) {
@@ -54,7 +45,7 @@ extern "C" int ah_attention_flash_bwd(const uint16_t* qkv, const uint16_t* O, co
         g.batch2 = batch;
         g.M = s; g.N = head_dim; g.K = s;
         g.A = dS; g.lda = s; g.a_s1 = s * s; g.a_s2 = (long long)heads * s * s;
-        g.a_mn_major = ah::gpt::flash_bwd_ds_transposed() ? 1 : 0;  // dS^T [key][query]
+        g.a_mn_major = 1;  // dS^T [key][query]
         g.B = qkv + h; g.b_mn_major = 1; g.ldb = 3 * h; g.b_s1 = head_dim; g.b_s2 = s * 3 * h;
         g.C = dqkv; g.ldc = 3 * h; g.c_s1 = head_dim; g.c_s2 = s * 3 * h;
         g.alpha = scale;

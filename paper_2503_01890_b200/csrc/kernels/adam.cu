@@ -2,9 +2,9 @@
 // proj/core/src/simulator.cpp:217-226, duration model workload.cpp:71).
 //
 // One pass over HBM per parameter: read bf16 grad (2 B) + fp32 master/m/v (12 B), write
-// fp32 master/m/v (12 B) + bf16 working copy (2 B) = 28 algorithmic bytes/param. The default
-// kernel (adam_tma_kernel) is a persistent CTA per SM fed by a TMA bulk-copy ring; the
-// register-streaming adam_vec_kernel serves capped-grid launches. Grad unscale is fused;
+// fp32 master/m/v (12 B) + bf16 working copy (2 B) = 28 algorithmic bytes/param. adam_tma_kernel
+// is a persistent CTA per SM fed by a TMA bulk-copy ring (a register-streaming variant measured
+// 5.39 vs 6.11 TB/s at 1 B params and was removed). Grad unscale is fused;
 // optional statistics (sum of squared unscaled grads, count of non-finite grads) are reduced
 // with warp shuffles inside a CTA and across CTAs in a fixed order by the last CTA to finish
 // (stats_commit: no float atomics, so the result is bitwise reproducible). An optional device-
@@ -106,93 +106,8 @@ __device__ __forceinline__ void block_stats_commit(float* stats, const Stat& st)
 }
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 2;
 
-struct F8 {
-    float x[8];
-};
-
-__device__ __forceinline__ void ld8(F8& d, const float* q) {
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(d.x[0]), "=f"(d.x[1]), "=f"(d.x[2]), "=f"(d.x[3])
-                 : "l"(q));
-    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(d.x[4]), "=f"(d.x[5]), "=f"(d.x[6]), "=f"(d.x[7])
-                 : "l"(q + 4));
-}
-__device__ __forceinline__ void st8(float* q, const F8& d) {
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(q), "f"(d.x[0]),
-                 "f"(d.x[1]), "f"(d.x[2]), "f"(d.x[3])
-                 : "memory");
-    asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(q + 4), "f"(d.x[4]),
-                 "f"(d.x[5]), "f"(d.x[6]), "f"(d.x[7])
-                 : "memory");
-}
-
-template <bool kWriteBf16, bool kStats>
-__global__ void __launch_bounds__(kThreads, 2)
-adam_vec_kernel(float* __restrict__ p, float* __restrict__ m, float* __restrict__ v,
-                const uint16_t* __restrict__ g, uint16_t* __restrict__ pout, size_t n_vec,
-                AdamScalars k, const int* __restrict__ skip, float* __restrict__ stats) {
-    if (skip != nullptr && *skip != 0) return;
-    Stat st;
-    const size_t stride = (size_t)gridDim.x * kThreads;
-    for (size_t base = (size_t)blockIdx.x * kThreads + threadIdx.x; base < n_vec;
-         base += stride * kUnroll) {
-        uint4 gv[kUnroll];
-        F8 pv[kUnroll], mv[kUnroll], vv[kUnroll];
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const size_t j = base + (size_t)u * stride;
-            if (j < n_vec) {
-                gv[u] = ld_stream_u4(g + j * 8);
-                ld8(pv[u], p + j * 8);
-                ld8(mv[u], m + j * 8);
-                ld8(vv[u], v + j * 8);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
-            const size_t j = base + (size_t)u * stride;
-            if (j >= n_vec) continue;
-            const uint32_t gw[4] = {gv[u].x, gv[u].y, gv[u].z, gv[u].w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                const uint32_t bits = (e & 1) ? (gw[e >> 1] >> 16) : (gw[e >> 1] & 0xffffu);
-                const float gf = __fmul_rn(bf16_bits_to_f32(bits), k.inv_scale);
-                if (kStats) account(st, gf);
-                adam_one(pv[u].x[e], mv[u].x[e], vv[u].x[e], gf, k);
-            }
-            st8(p + j * 8, pv[u]);
-            st8(m + j * 8, mv[u]);
-            st8(v + j * 8, vv[u]);
-            if (kWriteBf16)
-                st_u4(pout + j * 8,
-                      make_uint4(pack_bf16x2(pv[u].x[0], pv[u].x[1]), pack_bf16x2(pv[u].x[2], pv[u].x[3]),
-                                 pack_bf16x2(pv[u].x[4], pv[u].x[5]), pack_bf16x2(pv[u].x[6], pv[u].x[7])));
-        }
-    }
-    if (kStats) {
-        __shared__ float s_sum[kThreads / 32];
-        __shared__ unsigned s_bad[kThreads / 32];
-        const float ws = warp_sum(st.sumsq);
-        const unsigned wb = warp_sum_u(st.nonfinite);
-        if ((threadIdx.x & 31) == 0) {
-            s_sum[threadIdx.x >> 5] = ws;
-            s_bad[threadIdx.x >> 5] = wb;
-        }
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            float a = threadIdx.x < kThreads / 32 ? s_sum[threadIdx.x] : 0.f;
-            unsigned b = threadIdx.x < kThreads / 32 ? s_bad[threadIdx.x] : 0u;
-            a = warp_sum(a);
-            b = warp_sum_u(b);
-            if (threadIdx.x == 0) stats_commit(stats, a, b);
-        }
-    }
-}
-
-// TMA-fed variant (the default): a persistent CTA per SM streams tiles of kTile params
+// The update kernel: a persistent CTA per SM streams tiles of kTile params
 // (p, m, v fp32 + g bf16 = 14 B/param) HBM -> shared memory with 1-D bulk copies
 // (cp.async.bulk ... mbarrier::complete_tx) issued by one producer thread into a kStages-deep
 // ring, so ~(kStages-1) x 28 KB of reads are in flight per SM independent of how many warps are
@@ -405,11 +320,7 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
     size_t done = 0;
     if (vec) {
         const size_t n_vec = a.n / 8;
-        static const bool use_tma = [] {
-            const char* e = std::getenv("AH_ADAM_KERNEL");
-            return !(e && e[0] == 'v');  // AH_ADAM_KERNEL=vec selects the register-streaming kernel
-        }();
-        if (n_vec && use_tma && a.max_ctas <= 0) {
+        if (n_vec) {
             const size_t tiles = (n_vec * 8 + kTile - 1) / kTile;
             const int grid = (int)(tiles < (size_t)kNumSMs ? tiles : (size_t)kNumSMs);
             static bool attr = [] {
@@ -429,18 +340,6 @@ cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
                 launch_ex((adam_tma_kernel<false, true>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
             else
                 launch_ex((adam_tma_kernel<false, false>), dim3(grid), dim3(kTmaThreads), kTmaSmem, stream, 1, a.p, a.m, a.v, a.g, a.p_bf16, nm, k, a.skip, a.stats);
-        } else if (n_vec) {
-            int grid = grid_for((n_vec + kUnroll - 1) / kUnroll, kThreads, 2);
-            if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
-            if (a.stats && grid > kStatsMaxCtas) grid = kStatsMaxCtas;
-            if (a.p_bf16 && a.stats)
-                adam_vec_kernel<true, true><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
-            else if (a.p_bf16)
-                adam_vec_kernel<true, false><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
-            else if (a.stats)
-                adam_vec_kernel<false, true><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
-            else
-                adam_vec_kernel<false, false><<<grid, kThreads, 0, stream>>>(a.p, a.m, a.v, a.g, a.p_bf16, n_vec, k, a.skip, a.stats);
         }
         done = n_vec * 8;
     }

@@ -1,27 +1,28 @@
-// Flash-style causal attention on tcgen05 (sm_100a): forward keeps only O and the per-row
-// log-sum-exp; backward recomputes P from Q, K and the log-sum-exp.
+// Flash-style causal attention on tcgen05 (sm_100a): the forward keeps only O and the per-row
+// log-sum-exp; the backward recomputes P from Q, K and the log-sum-exp.
 //
-// Forward, one CTA per (128-query tile, head, sequence), heavy (long causal) tiles first:
-//   S_j = Q K_j^T            tcgen05.mma into a double-buffered TMEM score tile
+// Forward (flash_fwd_pk_kernel): persistent, one CTA per SM over snake-ordered (128-query tile,
+// head, sequence) items, heavy (long causal) items first:
+//   S_j = Q K_j^T            tcgen05.mma into one of two TMEM score buffers
 //   online softmax            8 warps: thread = query row, warp pair (w, w + 4) splits the 128
 //                             keys of a tile; the pair exchanges its tile max through smem
-//   O += P_j V_j              P_j (bf16) staged in smem as the A operand, O accumulated in TMEM
+//   O += P_j V_j              P_j (bf16) written back into its score buffer, A read from TMEM
 // Softmax runs in the log2 domain on raw scores, p = 2^(S * scale * log2e - m * scale * log2e),
 // with lazy rescaling: the running max m only moves (and O / l are rescaled in TMEM) when the
-// tile max exceeds it by more than 2^8, so most tiles touch O only through the MMA. Output
-// O / l and lse2 = m * scale * log2e + log2(l) per row (the backward's softmax statistics).
+// tile max exceeds it by more than 2^8. Output O / l and lse2 = m * scale * log2e + log2(l) per
+// row (the backward's softmax statistics).
 //
-// Backward, one CTA per (128-key tile, head, sequence), query tiles i >= key tile:
-//   S_i = Q_i K^T, P_i = 2^(S_i * scale * log2e - lse2_i)     (recomputed, never stored)
-//   dP_i = dO_i V^T; dS_i = P_i * (dP_i - D_i)                (D = rowsum(dO * O))
-//   dV += P_i^T dO_i, dK += dS_i^T Q_i                        (TMEM accumulators)
-// dS_i also goes to HBM for the deterministic dQ = dS K GEMM (no cross-CTA atomics).
-// P_i and dS_i share one smem tile (dS overwrites P once the dV MMA has read it).
+// Backward (flash_bwd_t_kernel): persistent over (128-key tile, head, sequence) items, scores
+// formed key-major so P^T and dS^T are the TMEM A operands of the dV / dK MMAs:
+//   S^T = K Q_i^T, P^T = 2^(S^T * scale * log2e - lse2_i)      (recomputed, never stored)
+//   dP^T = V dO_i^T; dS^T = P^T * (dP^T - D_i)                 (D = rowsum(dO * O))
+//   dV += P^T dO_i, dK += dS^T Q_i                             (TMEM accumulators)
+// dS^T also goes to HBM for the deterministic dQ = dS K GEMM (no cross-CTA atomics).
 //
 // Operand staging: every tile is a K-major SWIZZLE_128B 128 x 128 bf16 box pair (two 64-column
-// atoms); read as the MN-major operand of its transpose it gives P^T, dS^T, V, dO, Q for free.
-// Warp roles (384 threads): 0 TMA producer, 1 MMA issuer (one thread), 2 TMEM allocator,
-// 4-11 softmax / epilogue. Shapes: head_dim = 128, seq_len % 128 == 0.
+// atoms); read as the MN-major operand of its transpose it gives V, dO, Q for free. Warp roles:
+// 0 TMA producer, 1 MMA issuer (one thread), 2 TMEM allocator, 4.. softmax / epilogue.
+// Shapes: head_dim = 128, seq_len % 128 == 0 (others take the unfused GEMM path, gpt_model.cpp).
 #include <cuda.h>
 
 #include <cstdlib>
@@ -79,204 +80,6 @@ struct FwdParams {
     float* lse2;      // [B][nh][s]
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
-flash_fwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const FwdParams A) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = align1024(smem_raw);
-    uint8_t* sQ = sm;
-    uint8_t* sK = sm + kTile;      // [2]
-    uint8_t* sV = sm + 3 * kTile;  // [2]
-    uint8_t* sP = sm + 5 * kTile;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kTile);
-    uint64_t* q_full = bar;
-    uint64_t* k_full = bar + 1;   // [2]
-    uint64_t* k_empty = bar + 3;  // [2]
-    uint64_t* v_full = bar + 5;   // [2]
-    uint64_t* v_empty = bar + 7;  // [2]
-    uint64_t* s_full = bar + 9;   // [2]
-    uint64_t* s_free = bar + 11;  // [2]
-    uint64_t* p_full = bar + 13;
-    uint64_t* p_free = bar + 14;
-    uint64_t* o_full = bar + 15;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 16);
-    float* xmax = reinterpret_cast<float*>(bar + 18);  // [2 parity][2 halves][128 rows]
-    float* xsum = xmax + 2 * 2 * 128;                  // [2 halves][128 rows]
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nqt = A.s / kT;
-    const int qt = nqt - 1 - (int)blockIdx.x;
-    const int head = blockIdx.y, b = blockIdx.z;
-    const int n = qt + 1;  // key tiles 0..qt
-
-    if (warp == 0 && lane == 0) {
-        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV})
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-        mbar_init(smem_u32(q_full), 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&k_full[i]), 1);
-            mbar_init(smem_u32(&k_empty[i]), 1);
-            mbar_init(smem_u32(&v_full[i]), 1);
-            mbar_init(smem_u32(&v_empty[i]), 1);
-            mbar_init(smem_u32(&s_full[i]), 1);
-            mbar_init(smem_u32(&s_free[i]), 8);
-        }
-        mbar_init(smem_u32(p_full), 8);
-        mbar_init(smem_u32(p_free), 1);
-        mbar_init(smem_u32(o_full), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    const uint32_t tmem = *tmem_holder;  // S[0] 0-127, S[1] 128-255, O 256-383
-
-    if (warp == 0) {
-        if (lane == 0) {  // ===== TMA producer =====
-            mbar_expect_tx(smem_u32(q_full), kTile);
-            load_tile(smem_u32(sQ), &tmQ, smem_u32(q_full), qt * kT, head, b);
-            for (int j = 0; j < n; ++j) {
-                const int st = j & 1;
-                const uint32_t ph = (j >> 1) & 1;
-                mbar_wait(smem_u32(&k_empty[st]), ph ^ 1);
-                mbar_expect_tx(smem_u32(&k_full[st]), kTile);
-                load_tile(smem_u32(sK + st * kTile), &tmK, smem_u32(&k_full[st]), j * kT, head, b);
-                mbar_wait(smem_u32(&v_empty[st]), ph ^ 1);
-                mbar_expect_tx(smem_u32(&v_full[st]), kTile);
-                load_tile(smem_u32(sV + st * kTile), &tmV, smem_u32(&v_full[st]), j * kT, head, b);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
-            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
-            constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (K-major) x V (MN-major)
-            mbar_wait(smem_u32(q_full), 0);
-            auto issue_S = [&](int j) {
-                const int st = j & 1;
-                const uint32_t ph = (j >> 1) & 1;
-                mbar_wait(smem_u32(&k_full[st]), ph);
-                mbar_wait(smem_u32(&s_free[st]), ph ^ 1);
-                fence_after();
-                const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + st * kTile);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + st * 128, kdesc(qa, t), kdesc(ka, t), idS, t > 0);
-                commit(smem_u32(&s_full[st]));
-                commit(smem_u32(&k_empty[st]));
-            };
-            issue_S(0);
-            for (int j = 0; j < n; ++j) {
-                if (j + 1 < n) issue_S(j + 1);  // scores of j+1 overlap the softmax of j
-                const int st = j & 1;
-                mbar_wait(smem_u32(p_full), j & 1);
-                mbar_wait(smem_u32(&v_full[st]), (j >> 1) & 1);
-                fence_after();
-                const uint32_t pa = smem_u32(sP), va = smem_u32(sV + st * kTile);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + 256, kdesc(pa, t), mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
-                commit(smem_u32(p_free));
-                commit(smem_u32(&v_empty[st]));
-            }
-            commit(smem_u32(o_full));
-        }
-    } else if (warp >= 4) {  // ===== online softmax / epilogue =====
-        const int half = (warp - 4) >> 2, quarter = warp & 3;
-        const int r = quarter * 32 + lane;
-        const int q = qt * kT + r;
-        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
-        const int pair_bar = 1 + quarter;  // named barrier of warps (quarter, quarter + 4)
-        const float sl2 = A.sl2;
-        float m_used = -INFINITY, l = 0.f;
-        for (int j = 0; j < n; ++j) {
-            const int st = j & 1;
-            mbar_wait(smem_u32(&s_full[st]), (j >> 1) & 1);
-            fence_after();
-            float v[64];
-            ld64(tmem + lane_base + st * 128 + half * 64, v);
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&s_free[st]));
-            if (j == qt) {  // diagonal tile: keys > q are masked
-                const int lim = q - j * kT - half * 64;
-#pragma unroll
-                for (int i = 0; i < 64; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
-            }
-            float cm = v[0];
-#pragma unroll
-            for (int i = 1; i < 64; ++i) cm = fmaxf(cm, v[i]);
-            xmax[(st * 2 + half) * 128 + r] = cm;
-            asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-            const float mt = fmaxf(cm, xmax[(st * 2 + (half ^ 1)) * 128 + r]);  // finite: key 0 <= q
-            float alpha = 1.f;
-            bool rescale = false;
-            if (m_used == -INFINITY) {
-                m_used = mt;
-            } else if ((mt - m_used) * sl2 > kRescaleLog2) {
-                alpha = ex2_approx((m_used - mt) * sl2);
-                l *= alpha;
-                m_used = mt;
-                rescale = true;
-            }
-            const float mb = m_used * sl2;
-            uint32_t w[32];
-            float add = 0.f;
-#pragma unroll
-            for (int i = 0; i < 32; ++i) {
-                const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
-                add += p0 + p1;
-                w[i] = pack_bf16x2_rn(p0, p1);
-            }
-            l += add;
-            if (j > 0) mbar_wait(smem_u32(p_free), (j - 1) & 1);  // P V of j-1 done: sP and O are ours
-            if (__any_sync(0xffffffffu, rescale)) {  // tcgen05.ld/st are warp-collective: alpha = 1 elsewhere
-                fence_after();
-#pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    float o[32];
-                    const uint32_t ta = tmem + lane_base + 256 + half * 64 + c * 32;
-                    ld32(ta, o);
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) o[i] *= alpha;
-                    st32(ta, o);
-                }
-            }
-            sts_row_half(sP, half, r, w);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // P visible to the tensor core
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(p_full));
-        }
-        xsum[half * 128 + r] = l;
-        asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory");
-        const float lt = l + xsum[(half ^ 1) * 128 + r];
-        const float inv = 1.f / lt;
-        if (half == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
-        mbar_wait(smem_u32(o_full), 0);
-        fence_after();
-        uint16_t* orow = A.O + ((size_t)b * A.s + q) * A.h + (size_t)head * kHD + half * 64;
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-            float v[32];
-            ld32(tmem + lane_base + 256 + half * 64 + c * 32, v);
-            uint4* op = reinterpret_cast<uint4*>(orow + c * 32);
-#pragma unroll
-            for (int k8 = 0; k8 < 4; ++k8)
-                op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
-                                    pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
-        }
-    }
-    fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-    }
-}
 
 // ---------------------------------------------------------------------------------------
 // Persistent forward (the default): one CTA per SM walks a snake-ordered list of
@@ -625,234 +428,10 @@ struct BwdParams {
     uint16_t* dqkv;     // [B][s][3h]
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
-flash_bwd_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                 const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                 const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = align1024(smem_raw);
-    uint8_t* sK = sm;
-    uint8_t* sV = sm + kTile;
-    uint8_t* sQ = sm + 2 * kTile;   // [2]
-    uint8_t* sdO = sm + 4 * kTile;  // [2]
-    uint8_t* sPS = sm + 6 * kTile;  // P_i, then dS_i
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kTile);
-    uint64_t* kv_full = bar;
-    uint64_t* st_full = bar + 1;   // [2]
-    uint64_t* st_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* s_free = bar + 6;
-    uint64_t* dp_full = bar + 7;
-    uint64_t* dp_free = bar + 8;
-    uint64_t* p_full = bar + 9;
-    uint64_t* pv_done = bar + 10;
-    uint64_t* ds_full = bar + 11;
-    uint64_t* ps_free = bar + 12;
-    uint64_t* acc_full = bar + 13;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 14);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nt = A.s / kT;
-    const int kt = (int)blockIdx.x;  // 0 = most query tiles first
-    const int head = blockIdx.y, b = blockIdx.z;
-    const int nq = nt - kt;          // query tiles kt .. nt-1
-
-    if (warp == 0 && lane == 0) {
-        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmdO})
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-        mbar_init(smem_u32(kv_full), 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&st_full[i]), 1);
-            mbar_init(smem_u32(&st_empty[i]), 1);
-        }
-        mbar_init(smem_u32(s_full), 1);
-        mbar_init(smem_u32(s_free), 8);
-        mbar_init(smem_u32(dp_full), 1);
-        mbar_init(smem_u32(dp_free), 8);
-        mbar_init(smem_u32(p_full), 8);
-        mbar_init(smem_u32(pv_done), 1);
-        mbar_init(smem_u32(ds_full), 8);
-        mbar_init(smem_u32(ps_free), 1);
-        mbar_init(smem_u32(acc_full), 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    const uint32_t tmem = *tmem_holder;  // S 0-127, dP 128-255, dV 256-383, dK 384-511
-
-    if (warp == 0) {
-        if (lane == 0) {  // ===== TMA producer =====
-            mbar_expect_tx(smem_u32(kv_full), 2 * kTile);
-            load_tile(smem_u32(sK), &tmK, smem_u32(kv_full), kt * kT, head, b);
-            load_tile(smem_u32(sV), &tmV, smem_u32(kv_full), kt * kT, head, b);
-            for (int i = 0; i < nq; ++i) {
-                const int st = i & 1, qi = kt + i;
-                mbar_wait(smem_u32(&st_empty[st]), ((i >> 1) & 1) ^ 1);
-                const uint32_t fb = smem_u32(&st_full[st]);
-                mbar_expect_tx(fb, 2 * kTile);
-                load_tile(smem_u32(sQ + st * kTile), &tmQ, fb, qi * kT, head, b);
-                load_tile(smem_u32(sdO + st * kTile), &tmdO, fb, qi * kT, head, b);
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
-            constexpr uint32_t idSS = idesc_bf16(128, 128, 0, 0);   // X (K-major) x Y^T (K-major)
-            constexpr uint32_t idACC = idesc_bf16(128, 128, 1, 1);  // X^T (MN-major) x Y (MN-major)
-            mbar_wait(smem_u32(kv_full), 0);
-            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), psa = smem_u32(sPS);
-            auto issue_S_dP = [&](int i) {  // S_i = Q_i K^T, dP_i = dO_i V^T
-                const int st = i & 1;
-                mbar_wait(smem_u32(&st_full[st]), (i >> 1) & 1);
-                mbar_wait(smem_u32(s_free), (i & 1) ^ 1);
-                fence_after();
-                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem, kdesc(qa, t), kdesc(ka, t), idSS, t > 0);
-                commit(smem_u32(s_full));
-                mbar_wait(smem_u32(dp_free), (i & 1) ^ 1);
-                fence_after();
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + 128, kdesc(da, t), kdesc(va, t), idSS, t > 0);
-                commit(smem_u32(dp_full));
-            };
-            issue_S_dP(0);
-            for (int i = 0; i < nq; ++i) {
-                const int st = i & 1;
-                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
-                mbar_wait(smem_u32(p_full), i & 1);
-                fence_after();
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + 256, mndesc(psa, t), mndesc(da, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
-                commit(smem_u32(pv_done));
-                if (i + 1 < nq) issue_S_dP(i + 1);  // the next tile's scores overlap this tile's dS
-                mbar_wait(smem_u32(ds_full), i & 1);
-                fence_after();
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + 384, mndesc(psa, t), mndesc(qa, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
-                commit(smem_u32(&st_empty[st]));
-                commit(smem_u32(ps_free));
-            }
-            commit(smem_u32(acc_full));
-        }
-    } else if (warp >= 4) {  // ===== P, dS; epilogue =====
-        const int half = (warp - 4) >> 2, quarter = warp & 3;  // keys [64 * half, 64 * half + 64)
-        const int r = quarter * 32 + lane;
-        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
-        const float sl2 = A.sl2;
-        const size_t row0 = ((size_t)b * A.nh + head) * A.s + (size_t)kt * kT + r;
-        float lse_n = A.lse2[row0], D_n = A.D[row0];  // row statistics, prefetched one tile ahead
-        uint8_t* slab = sPS + half * (kTile / 2) + quarter * 4096;  // this warp's 32 rows x 64 keys
-        for (int i = 0; i < nq; ++i) {
-            const int qi = kt + i;
-            const int q = qi * kT + r;
-            const size_t row = row0 + (size_t)i * kT;
-            const float lse = lse_n, Dq = D_n;
-            if (i + 1 < nq) {
-                lse_n = A.lse2[row + kT];
-                D_n = A.D[row + kT];
-            }
-            mbar_wait(smem_u32(s_full), i & 1);
-            fence_after();
-            uint32_t w[32];
-            {
-                float v[64];
-                ld64(tmem + lane_base + half * 64, v);
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(s_free));
-#pragma unroll
-                for (int k = 0; k < 32; ++k)
-                    w[k] = pack_bf16x2_rn(ex2_approx(fmaf(v[2 * k], sl2, -lse)), ex2_approx(fmaf(v[2 * k + 1], sl2, -lse)));
-            }
-            if (qi == kt) {  // diagonal tile: keys > q have P = 0
-                const int lim = q - kt * kT - half * 64;
-#pragma unroll
-                for (int k = 0; k < 32; ++k)
-                    w[k] &= (2 * k <= lim ? 0x0000ffffu : 0u) | (2 * k + 1 <= lim ? 0xffff0000u : 0u);
-            }
-            if (i > 0) {
-                mbar_wait(smem_u32(ps_free), (i - 1) & 1);  // dK MMA of i-1 has read dS
-                if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // and the dS store
-                __syncwarp();
-            }
-            sts_row_half(sPS, half, r, w);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(p_full));
-            mbar_wait(smem_u32(dp_full), i & 1);
-            fence_after();
-            uint32_t o[32];
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                float v[32];
-                ld32(tmem + lane_base + 128 + half * 64 + c * 32, v);
-#pragma unroll
-                for (int k = 0; k < 16; ++k) {
-                    const uint32_t pw = w[c * 16 + k];
-                    const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
-                    o[c * 16 + k] = pack_bf16x2_rn(p0 * (v[2 * k] - Dq), p1 * (v[2 * k + 1] - Dq));
-                }
-            }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(dp_free));
-            mbar_wait(smem_u32(pv_done), i & 1);  // dV MMA has read P
-            sts_row_half(sPS, half, r, o);
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(smem_u32(ds_full));
-                // this warp's 32 x 64 dS slab -> HBM (the smem slab is the box's SWIZZLE_128B image)
-                asm volatile(
-                    "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                        reinterpret_cast<uint64_t>(&tmdS)),
-                    "r"(smem_u32(slab)), "r"(kt * kT + half * 64), "r"(qi * kT + quarter * 32), "r"(head), "r"(b)
-                    : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-            }
-        }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-        mbar_wait(smem_u32(acc_full), 0);
-        fence_after();
-        // thread r = key row of the tile: dV, dK (x scale) -> dqkv
-        uint16_t* base = A.dqkv + ((size_t)b * A.s + (size_t)kt * kT + r) * 3 * A.h + (size_t)head * kHD + half * 64;
-#pragma unroll 1
-        for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
-            uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
-            const float f = which == 0 ? 1.f : A.scale;
-#pragma unroll 1
-            for (int c = 0; c < 2; ++c) {
-                float v[32];
-                ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
-                uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8)
-                    op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
-                                        pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
-            }
-        }
-    }
-    fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-    }
-}
 
 // ---------------------------------------------------------------------------------------
-// Persistent backward (the default): one CTA per SM walks a snake-ordered list of
-// (key tile, head, sequence) items, heavy (many query tiles) first. The Q / dO ring, the row
-// statistics and the S / dP / P-dS pipeline continue across item boundaries; the next item's
-// K / V load as soon as the current item's last S / dP MMAs have read K / V, and its first S / dP
-// MMAs are issued while the epilogue warps drain the current item's dV / dK accumulators.
+// Persistent backward schedule: one CTA per SM walks a snake-ordered list of (key tile, head,
+// sequence) items, heavy (many query tiles) first.
 struct BwdItems {
     int nt, nh, B, total, G, c;
     __device__ int count() const {
@@ -871,265 +450,6 @@ struct BwdItems {
     }
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
-flash_bwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmdO,
-                    const __grid_constant__ CUtensorMap tmdS, const BwdParams A) {
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* sm = align1024(smem_raw);
-    uint8_t* sK = sm;
-    uint8_t* sV = sm + kTile;
-    uint8_t* sQ = sm + 2 * kTile;   // [2]
-    uint8_t* sdO = sm + 4 * kTile;  // [2]
-    uint8_t* sPS = sm + 6 * kTile;  // P_i, then dS_i
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 7 * kTile);
-    uint64_t* kv_full = bar;
-    uint64_t* st_full = bar + 1;   // [2]
-    uint64_t* st_empty = bar + 3;  // [2]
-    uint64_t* s_full = bar + 5;
-    uint64_t* s_free = bar + 6;
-    uint64_t* dp_full = bar + 7;
-    uint64_t* dp_free = bar + 8;
-    uint64_t* p_full = bar + 9;
-    uint64_t* pv_done = bar + 10;
-    uint64_t* ds_full = bar + 11;
-    uint64_t* ps_free = bar + 12;
-    uint64_t* acc_full = bar + 13;
-    uint64_t* kv_empty = bar + 14;
-    uint64_t* acc_free = bar + 15;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 16);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nt = A.s / kT;
-    BwdItems items{nt, A.nh, A.B, nt * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
-    const int n_items = items.count();
-
-    if (warp == 0 && lane == 0) {
-        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV, &tmdO})
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-        mbar_init(smem_u32(kv_full), 1);
-        mbar_init(smem_u32(kv_empty), 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&st_full[i]), 1);
-            mbar_init(smem_u32(&st_empty[i]), 1);
-        }
-        mbar_init(smem_u32(s_full), 1);
-        mbar_init(smem_u32(s_free), 8);
-        mbar_init(smem_u32(dp_full), 1);
-        mbar_init(smem_u32(dp_free), 8);
-        mbar_init(smem_u32(p_full), 8);
-        mbar_init(smem_u32(pv_done), 1);
-        mbar_init(smem_u32(ds_full), 8);
-        mbar_init(smem_u32(ps_free), 1);
-        mbar_init(smem_u32(acc_full), 1);
-        mbar_init(smem_u32(acc_free), 8);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 2) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(512));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    fence_before();
-    __syncthreads();
-    fence_after();
-    const uint32_t tmem = *tmem_holder;  // S 0-127, dP 128-255, dV 256-383, dK 384-511
-
-    if (warp == 0) {
-        if (lane == 0) {  // ===== TMA producer =====
-            uint32_t g = 0;
-            for (int it = 0; it < n_items; ++it) {
-                int kt, head, b;
-                items.get(it, kt, head, b);
-                if (it > 0) mbar_wait(smem_u32(kv_empty), (it - 1) & 1);  // last S / dP of it-1 read K, V
-                mbar_expect_tx(smem_u32(kv_full), 2 * kTile);
-                load_tile(smem_u32(sK), &tmK, smem_u32(kv_full), kt * kT, head, b);
-                load_tile(smem_u32(sV), &tmV, smem_u32(kv_full), kt * kT, head, b);
-                for (int qi = kt; qi < nt; ++qi, ++g) {
-                    const int st = g & 1;
-                    mbar_wait(smem_u32(&st_empty[st]), ((g >> 1) & 1) ^ 1);
-                    const uint32_t fb = smem_u32(&st_full[st]);
-                    mbar_expect_tx(fb, 2 * kTile);
-                    load_tile(smem_u32(sQ + st * kTile), &tmQ, fb, qi * kT, head, b);
-                    load_tile(smem_u32(sdO + st * kTile), &tmdO, fb, qi * kT, head, b);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ===== MMA issuer =====
-            constexpr uint32_t idSS = idesc_bf16(128, 128, 0, 0);   // X (K-major) x Y^T (K-major)
-            constexpr uint32_t idACC = idesc_bf16(128, 128, 1, 1);  // X^T (MN-major) x Y (MN-major)
-            const uint32_t ka = smem_u32(sK), va = smem_u32(sV), psa = smem_u32(sPS);
-            // S_g = Q_g K^T, dP_g = dO_g V^T; `first` = first tile of item `it` (waits its K / V);
-            // `last` = last tile of its item (K / V free once these MMAs complete)
-            auto issue_S_dP = [&](uint32_t g, int it, bool first, bool last) {
-                const int st = g & 1;
-                if (first) mbar_wait(smem_u32(kv_full), it & 1);
-                mbar_wait(smem_u32(&st_full[st]), (g >> 1) & 1);
-                mbar_wait(smem_u32(s_free), (g & 1) ^ 1);
-                fence_after();
-                const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem, kdesc(qa, t), kdesc(ka, t), idSS, t > 0);
-                commit(smem_u32(s_full));
-                mbar_wait(smem_u32(dp_free), (g & 1) ^ 1);
-                fence_after();
-#pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + 128, kdesc(da, t), kdesc(va, t), idSS, t > 0);
-                commit(smem_u32(dp_full));
-                if (last) commit(smem_u32(kv_empty));
-            };
-            uint32_t g = 0;
-            if (n_items > 0) {
-                int kt0, h0, b0;
-                items.get(0, kt0, h0, b0);
-                issue_S_dP(0, 0, true, kt0 == nt - 1);
-            }
-            for (int it = 0; it < n_items; ++it) {
-                int kt, head, b;
-                items.get(it, kt, head, b);
-                const int nq = nt - kt;
-                if (it > 0) mbar_wait(smem_u32(acc_free), (it - 1) & 1);  // epilogue of it-1 read dV / dK
-                for (int i = 0; i < nq; ++i, ++g) {
-                    const int st = g & 1;
-                    const uint32_t qa = smem_u32(sQ + st * kTile), da = smem_u32(sdO + st * kTile);
-                    mbar_wait(smem_u32(p_full), g & 1);
-                    fence_after();
-#pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        mma_f16(tmem + 256, mndesc(psa, t), mndesc(da, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
-                    commit(smem_u32(pv_done));
-                    if (i + 1 < nq) issue_S_dP(g + 1, it, false, i + 2 == nq);  // overlaps this tile's dS
-                    mbar_wait(smem_u32(ds_full), g & 1);
-                    fence_after();
-#pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        mma_f16(tmem + 384, mndesc(psa, t), mndesc(qa, t), idACC, (i > 0 || t > 0) ? 1u : 0u);
-                    commit(smem_u32(&st_empty[st]));
-                    commit(smem_u32(ps_free));
-                }
-                commit(smem_u32(acc_full));
-                if (it + 1 < n_items) {  // next item's first scores overlap this item's epilogue
-                    int kn, hn, bn;
-                    items.get(it + 1, kn, hn, bn);
-                    issue_S_dP(g, it + 1, true, kn == nt - 1);
-                }
-            }
-        }
-    } else if (warp >= 4) {  // ===== P, dS; epilogue =====
-        const int half = (warp - 4) >> 2, quarter = warp & 3;  // keys [64 * half, 64 * half + 64)
-        const int r = quarter * 32 + lane;
-        const uint32_t lane_base = uint32_t(quarter * 32) << 16;
-        const float sl2 = A.sl2;
-        uint8_t* slab = sPS + half * (kTile / 2) + quarter * 4096;  // this warp's 32 rows x 64 keys
-        uint32_t g = 0;
-        for (int it = 0; it < n_items; ++it) {
-            int kt, head, b;
-            items.get(it, kt, head, b);
-            const int nq = nt - kt;
-            const size_t row0 = ((size_t)b * A.nh + head) * A.s + (size_t)kt * kT + r;
-            float lse_n = A.lse2[row0], D_n = A.D[row0];  // row statistics, prefetched one tile ahead
-            for (int i = 0; i < nq; ++i, ++g) {
-                const int qi = kt + i;
-                const int q = qi * kT + r;
-                const size_t row = row0 + (size_t)i * kT;
-                const float lse = lse_n, Dq = D_n;
-                if (i + 1 < nq) {
-                    lse_n = A.lse2[row + kT];
-                    D_n = A.D[row + kT];
-                }
-                mbar_wait(smem_u32(s_full), g & 1);
-                fence_after();
-                uint32_t w[32];
-                {
-                    float v[64];
-                    ld64(tmem + lane_base + half * 64, v);
-                    fence_before();
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(smem_u32(s_free));
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        w[k] = pack_bf16x2_rn(ex2_approx(fmaf(v[2 * k], sl2, -lse)), ex2_approx(fmaf(v[2 * k + 1], sl2, -lse)));
-                }
-                if (qi == kt) {  // diagonal tile: keys > q have P = 0
-                    const int lim = q - kt * kT - half * 64;
-#pragma unroll
-                    for (int k = 0; k < 32; ++k)
-                        w[k] &= (2 * k <= lim ? 0x0000ffffu : 0u) | (2 * k + 1 <= lim ? 0xffff0000u : 0u);
-                }
-                if (g > 0) {
-                    mbar_wait(smem_u32(ps_free), (g - 1) & 1);  // dK MMA of g-1 has read dS
-                    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // and the dS store
-                    __syncwarp();
-                }
-                sts_row_half(sPS, half, r, w);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(p_full));
-                mbar_wait(smem_u32(dp_full), g & 1);
-                fence_after();
-                uint32_t o[32];
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    float v[32];
-                    ld32(tmem + lane_base + 128 + half * 64 + c * 32, v);
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const uint32_t pw = w[c * 16 + k];
-                        const float p0 = __uint_as_float(pw << 16), p1 = __uint_as_float(pw & 0xffff0000u);
-                        o[c * 16 + k] = pack_bf16x2_rn(p0 * (v[2 * k] - Dq), p1 * (v[2 * k + 1] - Dq));
-                    }
-                }
-                fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(dp_free));
-                mbar_wait(smem_u32(pv_done), g & 1);  // dV MMA has read P
-                sts_row_half(sPS, half, r, o);
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(smem_u32(ds_full));
-                    asm volatile(
-                        "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                            reinterpret_cast<uint64_t>(&tmdS)),
-                        "r"(smem_u32(slab)), "r"(kt * kT + half * 64), "r"(qi * kT + quarter * 32), "r"(head), "r"(b)
-                        : "memory");
-                    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                }
-            }
-            mbar_wait(smem_u32(acc_full), it & 1);
-            fence_after();
-            // thread r = key row of the tile: dV, dK (x scale) -> dqkv
-            uint16_t* base = A.dqkv + ((size_t)b * A.s + (size_t)kt * kT + r) * 3 * A.h + (size_t)head * kHD + half * 64;
-#pragma unroll 1
-            for (int which = 0; which < 2; ++which) {  // 0: dV (col 256), 1: dK (col 384)
-                uint16_t* dst = base + (which == 0 ? 2 * A.h : A.h);
-                const float f = which == 0 ? 1.f : A.scale;
-#pragma unroll 1
-                for (int c = 0; c < 2; ++c) {
-                    float v[32];
-                    ld32(tmem + lane_base + 256 + which * 128 + half * 64 + c * 32, v);
-                    uint4* op = reinterpret_cast<uint4*>(dst + c * 32);
-#pragma unroll
-                    for (int k8 = 0; k8 < 4; ++k8)
-                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * f, v[8 * k8 + 1] * f), pack_bf16x2_rn(v[8 * k8 + 2] * f, v[8 * k8 + 3] * f),
-                                            pack_bf16x2_rn(v[8 * k8 + 4] * f, v[8 * k8 + 5] * f), pack_bf16x2_rn(v[8 * k8 + 6] * f, v[8 * k8 + 7] * f));
-                }
-            }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(acc_free));
-        }
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-    }
-    fence_before();
-    __syncthreads();
-    if (warp == 2) {
-        fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
-    }
-}
 
 // ---------------------------------------------------------------------------------------
 // Transposed persistent backward (the default). Per (key tile, head, sequence) item and query
@@ -1469,6 +789,36 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
     }
 }
 
+// D[b][head][q] = sum_c dO[b, q, head*hd + c] * O[b, q, head*hd + c]. Half a warp per
+// (b, q, head) row: 16 lanes x 16-byte loads cover the 128 head columns; grid-stride.
+__global__ void attn_bwd_dot_kernel(const uint16_t* __restrict__ dO, const uint16_t* __restrict__ O, float* __restrict__ D,
+                                    int B, int s, int nh) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const long long rows = (long long)B * s * nh;
+    const int sub = threadIdx.x & 15;
+    for (long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 4; w < rows;
+         w += ((long long)gridDim.x * blockDim.x) >> 4) {
+        const size_t off = (size_t)w * kHD + sub * 8;  // (b*s + q)*h + head*hd == w*hd
+        const uint4 a = *reinterpret_cast<const uint4*>(dO + off);
+        const uint4 o = *reinterpret_cast<const uint4*>(O + off);
+        const uint32_t au[4] = {a.x, a.y, a.z, a.w}, ou[4] = {o.x, o.y, o.z, o.w};
+        float t = 0.f;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            t += bf16_bits_to_f32(au[k] & 0xffffu) * bf16_bits_to_f32(ou[k] & 0xffffu) +
+                 bf16_bits_to_f32(au[k] >> 16) * bf16_bits_to_f32(ou[k] >> 16);
+#pragma unroll
+        for (int o2 = 8; o2 > 0; o2 >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o2);
+        if (sub == 0) {
+            const int head = (int)(w % nh);
+            const long long bq = w / nh;  // b * s + q
+            const long long bb = bq / s, q = bq % s;
+            D[(bb * nh + head) * s + q] = t;
+        }
+    }
+}
+
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1535,18 +885,10 @@ cudaError_t set_smem(K kernel, size_t bytes, bool& done) {
 
 bool flash_supported(int hd, int s) { return hd == kHD && s % kT == 0 && s >= kT; }
 
-// AH_FLASH_BWD=v1: one CTA per (key tile, head, sequence); =pk: persistent, query-major scores
-// (dS [q][k]); default: persistent transposed (dS^T [k][q]).
-int flash_bwd_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("AH_FLASH_BWD");
-        if (e && e[0] == 'v' && e[1] == '1') return 0;
-        if (e && e[0] == 'p' && e[1] == 'k') return 1;
-        return 2;
-    }();
-    return v;
+cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st) {
+    launch_ex(attn_bwd_dot_kernel, dim3(kNumSMs * 8), dim3(256), 0, st, 1, dO, O, D, B, s, nh);
+    return launched(1);
 }
-bool flash_bwd_ds_transposed() { return flash_bwd_variant() == 2; }
 
 cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
                       cudaStream_t st) {
@@ -1564,42 +906,16 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     a.sl2 = scale * 1.4426950408889634f;
     a.O = O;
     a.lse2 = lse2;
-    static const bool v1 = [] {
-        const char* e = std::getenv("AH_FLASH_FWD");
-        return e && e[0] == 'v' && e[1] == '1';  // AH_FLASH_FWD=v1: one CTA per (tile, head, sequence)
-    }();
-    if (v1) {
-        const size_t smem = 1024 + 6 * (size_t)kTile + 18 * 8 + 6 * 128 * 4;
-        static bool cfg = false;
-        cudaError_t e = set_smem(flash_fwd_kernel, smem, cfg);
-        if (e != cudaSuccess) return e;
-        flash_fwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, a);
-        return launched(1);
-    }
-    // default: 8 softmax warps (64 keys each, 63 us at B=8 s=1024 16 heads); AH_FLASH_FWD=pk4:
-    // 16 softmax warps (32 keys each, 66 us) — the softmax warps are not the limiter
-    static const int parts = [] {
-        const char* e = std::getenv("AH_FLASH_FWD");
-        return (e && e[0] == 'p' && e[1] == 'k' && e[2] == '4') ? 4 : 2;
-    }();
     const int items = (s / kT) * nh * B;
     const int grid = items < kNumSMs ? items : kNumSMs;
     CUtensorMap mo;  // O [B*s][h], box 32 x 32, SWIZZLE_64B (the epilogue slabs)
     if (!rows_view(&mo, O, h, (long long)B * s, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
     // tiles | barriers (1 KB) | epilogue slabs (2 KB per softmax warp)
-    if (parts == 2) {
-        const size_t smem = 1024 + 6 * (size_t)kTile + 1024 + 8 * 2048;
-        static bool cfg2 = false;
-        cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg2);
-        if (e != cudaSuccess) return e;
-        launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, mo, a);
-        return launched(1);
-    }
-    const size_t smem = 1024 + 6 * (size_t)kTile + 24 * 8;
-    static bool cfg4 = false;
-    cudaError_t e = set_smem(flash_fwd_pk_kernel<4>, smem, cfg4);
+    const size_t smem = 1024 + 6 * (size_t)kTile + 1024 + 8 * 2048;
+    static bool cfg = false;
+    cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg);
     if (e != cudaSuccess) return e;
-    flash_fwd_pk_kernel<4><<<grid, (4 + 16) * 32, smem, st>>>(mq, mk, mv, mo, a);
+    launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, mo, a);
     return launched(1);
 }
 
@@ -1625,34 +941,17 @@ cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO
     a.D = D;
     a.dS = dS;
     a.dqkv = dqkv;
-    const int variant = flash_bwd_variant();
-    if (variant == 2) {  // transposed persistent kernel: dS^T [B][nh][key][query]
-        // tiles | lse/D stages (2 KB) | barriers (<= 1 KB) | 8 dS^T slabs (32 KB): the 227 KB maximum
-        const size_t smem = 6 * (size_t)kTile + 3072 + 8 * 4096;
-        static bool cfg3 = false;
-        e = set_smem(flash_bwd_t_kernel, smem, cfg3);
-        if (e != cudaSuccess) return e;
-        const int items = (s / kT) * nh * B;
-        CUtensorMap mdqkv;  // [B*s][3h] bf16, box 64 columns x 32 rows (the dV / dK slabs)
-        if (!rows_view(&mdqkv, dqkv, 3ll * h, (long long)B * s)) return cudaErrorInvalidValue;
-        launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, mds,
-                  mdqkv, a);
-        return launched(1);
-    }
-    if (variant == 0) {
-        const size_t smem = 1024 + 7 * (size_t)kTile + 16 * 8;
-        static bool cfg = false;
-        e = set_smem(flash_bwd_kernel, smem, cfg);
-        if (e != cudaSuccess) return e;
-        flash_bwd_kernel<<<dim3(s / kT, nh, B), kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
-        return launched(1);
-    }
-    const size_t smem = 1024 + 7 * (size_t)kTile + 18 * 8;
-    static bool cfg2 = false;
-    e = set_smem(flash_bwd_pk_kernel, smem, cfg2);
+    // transposed persistent kernel: dS^T [B][nh][key][query]
+    // tiles | lse/D stages (2 KB) | barriers (<= 1 KB) | 8 dS^T slabs (32 KB): the 227 KB maximum
+    const size_t smem = 6 * (size_t)kTile + 3072 + 8 * 4096;
+    static bool cfg3 = false;
+    e = set_smem(flash_bwd_t_kernel, smem, cfg3);
     if (e != cudaSuccess) return e;
     const int items = (s / kT) * nh * B;
-    flash_bwd_pk_kernel<<<items < kNumSMs ? items : kNumSMs, kThreads, smem, st>>>(mq, mk, mv, mdo, mds, a);
+    CUtensorMap mdqkv;  // [B*s][3h] bf16, box 64 columns x 32 rows (the dV / dK slabs)
+    if (!rows_view(&mdqkv, dqkv, 3ll * h, (long long)B * s)) return cudaErrorInvalidValue;
+    launch_ex(flash_bwd_t_kernel, dim3(items < kNumSMs ? items : kNumSMs), dim3(kThreads), smem, st, 1, mq, mk, mv, mdo, mds,
+              mdqkv, a);
     return launched(1);
 }
 

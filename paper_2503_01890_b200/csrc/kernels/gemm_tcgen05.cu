@@ -10,16 +10,21 @@
 // contiguous) so fwd (TN), dgrad (TT) and wgrad (NN) run without transposes. z indexes a
 // two-level batch (e.g. head x sequence) addressed through 4-D TMA tensor maps.
 //
-// Structure (one CTA per SM, persistent over output tiles, 256 threads):
-//   warp 0      TMA producer: 128x64 A tile + BNx64 B tile per stage, SWIZZLE_128B,
-//               STAGES-deep smem ring guarded by full/empty mbarriers
-//   warp 1      MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16
-//               (M=128, N=BN, K=16) x4 per stage into a TMEM accumulator; commits free the
-//               smem stage; a commit per tile hands the accumulator to the epilogue
-//   warp 2      TMEM allocator (2 x BN fp32 columns: double-buffered accumulator so the
+// Structure (persistent over output tiles, 384 threads = 12 warps; for BN = 256 two CTAs of a
+// cluster pair form one 256 x 256 tile with tcgen05.mma.cta_group::2, M = 256):
+//   warps 0-7   epilogue, two per TMEM lane quarter: tcgen05.ld 32x32b -> registers -> alpha /
+//               beta*C / bias / GELU (+ pre-activation aux) / GELU' / residual -> bf16 packs
+//               -> per-warp 32 x 32 smem slab -> TMA bulk tensor store (fp32 C: direct stores)
+//   warp 8      TMA producer: 128 x 64 A tile + B tile (its half under cta_group::2) per
+//               stage, SWIZZLE_128B, STAGES-deep smem ring guarded by full/empty mbarriers
+//   warp 9      MMA issuer: one elected thread issues tcgen05.mma (K = 16) x4 per stage into
+//               a TMEM accumulator; commits free the smem stage; a commit per tile hands the
+//               accumulator to the epilogue
+//   warp 10     TMEM allocator (2 x BN fp32 columns: double-buffered accumulator so the
 //               epilogue of tile i overlaps the MMAs of tile i+1)
-//   warps 4-7   epilogue: tcgen05.ld 32x32b -> registers -> alpha / beta*C / bias /
-//               GELU (+ pre-activation aux) / residual -> bf16 or fp32 global stores
+// The single-thread producer / MMA roles take the highest warp ids (the sub-partition arbiter
+// issues highest-warp-id first). A poorly filled last wave is split in K halves across CTA
+// pairs (stream-K), with fixed-order partial sums (deterministic).
 // Causal modes skip work that a causal mask zeroes: whole tiles above the diagonal, or the
 // K range of a tile (P·V, dS·K, dS^T·Q, P^T·dO).
 #include <cuda.h>
@@ -74,9 +79,6 @@ struct Params {
     int vec16_c, vec16_aux;  // 16-byte rows (direct path)
     int staged;              // smem-transposed epilogue (fp32 outputs)
     int vec_bias, vec16_res;  // 16-byte vector loads legal for bias / residual
-    int wait_ns;              // AH_GEMM_WAIT_NS: suspend-time hint of the producer / epilogue waits (0)
-    int mma_wait_ns;          // AH_GEMM_MMA_WAIT_NS: same for the MMA issuer's waits (0)
-    int dbg_no_store;         // AH_GEMM_DEBUG_NO_STORE (profiling only): 1 no epilogue, 2 no C store, 3 packs only
     int tma_c;                // bf16 C written by TMA bulk stores from smem slabs
     int fast;                 // tma_c, alpha 1, beta 0, N % BN == 0, 16-byte operand rows: lean epilogue
     int sk;                   // stream-K work split (CS == 1, non-causal)
@@ -424,7 +426,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
-                    mbar_wait_hint(smem_u32(&empty[stage]), phase ^ 1, (uint32_t)P.wait_ns);
+                    mbar_wait_hint(smem_u32(&empty[stage]), phase ^ 1, 0u);
                     const uint32_t a_dst = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_dst = smem_u32(sB + stage * B_BYTES);
                     const int k0 = kb * BK;
@@ -493,11 +495,11 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             for (int si = 0; si < nseg; ++si) {
                 const Tile T = segment<CS>(P, si, BN, crank);
                 if (T.skip) continue;
-                mbar_wait_hint(smem_u32(&tempty[acc]), acc_phase ^ 1, (uint32_t)P.mma_wait_ns);  // latency-critical
+                mbar_wait_hint(smem_u32(&tempty[acc]), acc_phase ^ 1, 0u);  // latency-critical
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = T.kb0; kb < T.kb1; ++kb) {
-                    mbar_wait_hint(smem_u32(&full[stage]), phase, (uint32_t)P.mma_wait_ns);
+                    mbar_wait_hint(smem_u32(&full[stage]), phase, 0u);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * B_BYTES);
@@ -549,7 +551,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         for (int si = 0; si < nseg; ++si) {
             const Tile T = segment<CS>(P, si, BN, crank);
             if (T.skip) continue;
-            mbar_wait_hint(smem_u32(&tfull[acc]), acc_phase, (uint32_t)P.wait_ns);
+            mbar_wait_hint(smem_u32(&tfull[acc]), acc_phase, 0u);
             tc_fence_after();
             if (T.role == 2) {  // stream-K suffix: wait for the previous CTA's partial of this tile
                 if (warp == 0 && lane == 0) {
@@ -589,7 +591,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         v[4 * w + 3] += x.w;
                     }
                 }
-                if (P.dbg_no_store == 1) continue;  // diagnostics: main loop only
                 if (P.fast && rows == 32) {
                     // Lean path for whole 32 x 32 chunks: vector operand loads, hardware bf16
                     // packs, one TMA store. (Its instruction count paces the MMAs: every issue
@@ -628,13 +629,6 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int w = 0; w < 4; ++w) add8(v, 8 * w, r4[w]);
                     }
                     uint8_t* slab = cstage + (warp * 2 + (epi_chunk & 1)) * 2048;
-                    if (P.dbg_no_store == 3) {  // diagnostics: packs only
-                        uint32_t x = 0;
-#pragma unroll
-                        for (int w = 0; w < 16; ++w) x ^= pack_bf16x2_rn(v[2 * w], v[2 * w + 1]);
-                        if (x == 0x12345678u) *reinterpret_cast<uint32_t*>(slab) = x;
-                        continue;
-                    }
                     if (epi_chunk >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
                     __syncwarp();
 #pragma unroll
@@ -644,7 +638,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                        pack_bf16x2_rn(v[8 * w + 4], v[8 * w + 5]), pack_bf16x2_rn(v[8 * w + 6], v[8 * w + 7]));
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     __syncwarp();
-                    if (lane == 0 && P.dbg_no_store != 2) {
+                    if (lane == 0) {
                         asm volatile(
                             "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
                                 reinterpret_cast<uint64_t>(&tmC)),
@@ -953,14 +947,6 @@ static bool make_map_sw(CUtensorMap* map, const void* base, long long inner, lon
            CUDA_SUCCESS;
 }
 
-static bool no_tma_store() {
-    static const bool v = [] {
-        const char* e = std::getenv("AH_GEMM_TMA_STORE");
-        return e && std::string(e) == "0";
-    }();
-    return v;
-}
-
 template <int BN, int STAGES, int CS>
 static size_t smem_bytes() {
     return 1024 + STAGES * (size_t)(BM * BK * 2 + (BN / CS) * BK * 2) + (2 * STAGES + 4) * 8 + 16 + kStagedSmem + 1024 + kEpiWarps * 2 * 2048;
@@ -1120,21 +1106,6 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         P.vec16_aux = (reinterpret_cast<uintptr_t>(g.aux) % 16 == 0) && g.ld_aux % 8 == 0 && g.aux_s1 % 8 == 0 &&
                       g.aux_s2 % 8 == 0;
         P.staged = 0;
-        static const int no_store = [] {  // 1: no epilogue, 2: no TMA store, 3: packs only
-            const char* e = std::getenv("AH_GEMM_DEBUG_NO_STORE");
-            return e ? std::atoi(e) : 0;
-        }();
-        P.dbg_no_store = no_store;
-        static const int wait_ns = [] {
-            const char* e = std::getenv("AH_GEMM_WAIT_NS");
-            return e ? std::atoi(e) : 0;
-        }();
-        P.wait_ns = wait_ns;
-        static const int mma_wait_ns = [] {
-            const char* e = std::getenv("AH_GEMM_MMA_WAIT_NS");
-            return e ? std::atoi(e) : 0;
-        }();
-        P.mma_wait_ns = mma_wait_ns;
         P.vec_bias = !g.bias_f32 && (reinterpret_cast<uintptr_t>(g.bias) % 16 == 0);
         P.vec16_res = (reinterpret_cast<uintptr_t>(g.residual) % 16 == 0) && g.ld_res % 8 == 0 && g.res_s1 % 8 == 0 &&
                       g.res_s2 % 8 == 0;
@@ -1143,24 +1114,16 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     // CTA pairs (cta_group::2, M = 256 over two adjacent M tiles sharing the B tile): each SM
     // stages and the MMA reads half of B, so smem traffic per k-block drops from 48 to 32 KB
     // and L2 -> SM traffic for B halves. Causal tiles have per-tile K ranges: unpaired.
-    static const bool no_cluster = [] {
-        const char* e = std::getenv("AH_GEMM_CLUSTER");
-        return e && std::string(e) == "1";
-    }();
-    // Stream-K when the data-parallel tile count fills the last wave poorly (e.g. 512 tiles on
-    // 148 SMs -> 86 % of 4 waves): every CTA then gets the same number of k-block iterations.
-    static const bool no_sk = [] {
-        const char* e = std::getenv("AH_GEMM_STREAMK");
-        return e && std::string(e) == "0";
-    }();
-    const int CS = (!no_cluster && BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
+    const int CS = (BN == 256 && g.causal == kCausalNone && P.tiles_m >= 2) ? 2 : 1;
     if (CS > 1) P.num_tiles = ((P.tiles_m + CS - 1) / CS) * P.tiles_n * P.batch1 * P.batch2;
     {
         const int G = kNumSMs / CS;  // clusters
         const int waves = (P.num_tiles + G - 1) / G;
         const double eff = (double)P.num_tiles / ((double)waves * G);
         const int tail = P.num_tiles - (P.num_tiles / G) * G;
-        P.sk = (!no_sk && (max_ctas <= 0 || max_ctas >= kNumSMs) && g.causal == kCausalNone && P.num_tiles >= G && eff < 0.9 && BN == 256 && tail > 0 &&
+        // Stream-K when the data-parallel tile count fills the last wave poorly (e.g. 512 tiles on
+        // 148 SMs -> 86 % of 4 waves): every CTA then gets the same number of k-block iterations.
+        P.sk = ((max_ctas <= 0 || max_ctas >= kNumSMs) && g.causal == kCausalNone && P.num_tiles >= G && eff < 0.9 && BN == 256 && tail > 0 &&
                 2 * tail <= G && P.k_blocks >= 64) ? 1 : 0;  // measured: +4% at K=8192, -2% at K=2048
     }
     if (P.sk) {
@@ -1202,7 +1165,7 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
     std::memset(&mc, 0, sizeof(mc));
     P.tma_c = 0;
     if (!g.c_f32 && (reinterpret_cast<uintptr_t>(g.C) % 16 == 0) && g.ldc % 8 == 0 && (P.batch1 == 1 || g.c_s1 % 8 == 0) &&
-        (P.batch2 == 1 || g.c_s2 % 8 == 0) && P.dbg_no_store != 1 && !no_tma_store())
+        (P.batch2 == 1 || g.c_s2 % 8 == 0))
         P.tma_c = make_map_sw(&mc, g.C, g.N, g.M, g.ldc, P.batch1, g.c_s1, P.batch2, g.c_s2, 32, 32,
                               CU_TENSOR_MAP_SWIZZLE_64B) ? 1 : 0;
     P.fast = P.tma_c && g.alpha == 1.f && g.beta == 0.f && P.N % BN == 0 &&

@@ -483,13 +483,9 @@ cudaError_t embed_fwd(const int* tok, const uint16_t* wte, const uint16_t* wpe, 
     return launched(1);
 }
 
-bool ln_rows_enabled(int h) {
-    static const bool on = [] {
-        const char* e = std::getenv("AH_LN");
-        return !(e && e[0] == 'w');  // AH_LN=warp selects the warp-per-row kernels
-    }();
-    return on && ln_rows_supported(h);
-}
+// The row-parallel kernels (ln_rows.cu) serve every h they support; the warp-per-row kernels
+// here are the fallback for the rest.
+bool ln_rows_enabled(int h) { return ln_rows_supported(h); }
 
 cudaError_t ln_fwd(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean, float* rstd,
                    int T, int h, cudaStream_t st) {

@@ -22,7 +22,8 @@ int reduce_chunks(int T);
 cudaError_t ln_bwd2(const uint16_t* dy, const uint16_t* x, const float* mean, const float* rstd, const uint16_t* g,
                     const uint16_t* dres, uint16_t* dx, uint16_t* dgdb, float* part, int T, int h, cudaStream_t st);
 // Row-parallel LayerNorm (ln_rows.cu): one CTA of h/8 threads per row chunk, rows read once.
-// ln_fwd / ln_bwd2 dispatch here when ln_rows_enabled(h) (h % 256 == 0; AH_LN=warp disables).
+// ln_fwd / ln_bwd2 dispatch here when ln_rows_enabled(h) (h % 256 == 0); the warp-per-row kernels
+// in gpt_kernels.cu are the fallback for other h.
 bool ln_rows_supported(int h);
 bool ln_rows_enabled(int h);
 cudaError_t ln_fwd_rows(const uint16_t* x, const uint16_t* g, const uint16_t* b, uint16_t* y, float* mean,
@@ -38,16 +39,6 @@ int colsum_rows(int T);
 cudaError_t colsum(const uint16_t* X, int T, int N, int ldx, float* part, void* out, int out_f32, cudaStream_t st);
 cudaError_t softmax_fwd(const float* S, uint16_t* P, long long rows, int s, cudaStream_t st);
 cudaError_t softmax_bwd(const uint16_t* P, const float* dP, uint16_t* dS, long long rows, int s, cudaStream_t st);
-// Fused causal attention forward (attn_fwd.cu): qkv [B, s, 3h] -> O [B, s, h] and the
-// normalised probabilities P [B, nh, s, s] (bf16, zero above the diagonal up to the tile end).
-bool attn_fwd_supported(int hd, int s);
-cudaError_t attn_fwd(const uint16_t* qkv, uint16_t* P, uint16_t* O, int B, int s, int nh, int hd, float scale,
-                     cudaStream_t st);
-// Fused causal attention backward (attn_bwd.cu): from qkv, O (= att), dO, P -> dS [B, nh, s, s]
-// (for the dQ GEMM) and dK (x scale), dV written into dqkv [B, s, 3h]; D: B*nh*s floats scratch.
-bool attn_bwd_supported(int hd, int s);
-cudaError_t attn_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const uint16_t* P, float* D,
-                     uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
 // D[b][head][q] = rowsum(dO * O) over the head's 128 columns (hd = 128).
 cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, int s, int nh, cudaStream_t st);
 // Flash attention (attn_flash.cu): single-pass online softmax forward that keeps only O and the
@@ -57,10 +48,8 @@ cudaError_t attn_rowdot(const uint16_t* dO, const uint16_t* O, float* D, int B, 
 bool flash_supported(int hd, int s);
 cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int s, int nh, int hd, float scale,
                       cudaStream_t st);
-// The default flash backward writes dS TRANSPOSED, dS^T [B, nh, s(key), s(query)]: the dQ GEMM
-// then reads it as an MN-major A operand. flash_bwd_ds_transposed() says which layout is used.
-int flash_bwd_variant();
-bool flash_bwd_ds_transposed();
+// The backward writes dS TRANSPOSED, dS^T [B, nh, s(key), s(query)]: the dQ GEMM reads it as an
+// MN-major A operand.
 cudaError_t flash_bwd(const uint16_t* qkv, const uint16_t* O, const uint16_t* dO, const float* lse2, float* D,
                       uint16_t* dS, uint16_t* dqkv, int B, int s, int nh, int hd, float scale, cudaStream_t st);
 // Register-resident single-read versions (attn_softmax.cu); fall back to the above for s > 2048.

@@ -18,9 +18,7 @@ struct AdamArgs {
     float decay, beta1, one_minus_beta1, beta2, one_minus_beta2, step_size, inv_sqrt_bc2, eps;
     float inv_scale = 1.f;
     const int* skip = nullptr;   // nullable device flag
-    float* stats = nullptr;      // nullable device [sumsq(float), nonfinite(uint32)]
-    int max_ctas = 0;            // > 0: register-streaming kernel on at most this many CTAs (runs beside
-                                 // a persistent GEMM on a side stream instead of taking every SM)
+    float* stats = nullptr;      // nullable AH_STATS_FLOATS buffer (include/autohete.h)
 };
 
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);

@@ -116,10 +116,6 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     check(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
     check(cudaEventCreateWithFlags(&ev_c2s_, cudaEventDisableTiming), "event");
     check(cudaEventCreateWithFlags(&ev_s2c_, cudaEventDisableTiming), "event");
-    {
-        const char* e = std::getenv("AH_PREFETCH_WEIGHTS");
-        prefetch_mat_ = !(e && e[0] == '0');
-    }
     check(cudaGetDevice(&device_), "get device");
     plan(cfg);
     allocate_and_init();
@@ -272,10 +268,6 @@ void Trainer::allocate_and_init() {
     check(cudaDeviceGetDefaultMemPool(&pool_, device_), "mempool");  // this rank's GPU, not GPU 0
     uint64_t thr = UINT64_MAX;
     check(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &thr), "mempool attr");
-    if (const char* e = std::getenv("AH_POOL_INTERNAL_DEPS")) {  // experiment knob: 0 = never make a
-        int on = std::atoi(e);                                     // stream wait on another lane's free
-        check(cudaMemPoolSetAttribute(pool_, cudaMemPoolReuseAllowInternalDependencies, &on), "mempool attr");
-    }
     size_t stat = 0;
     auto dalloc = [&](void** p, size_t bytes) {
         check(cudaMalloc(p, bytes), "cudaMalloc");
@@ -389,8 +381,6 @@ void Trainer::allocate_and_init() {
 // releases memory (release threshold = max), so the first deeply pipelined iterations do not
 // pay the driver's physical-allocation path inside the timed region.
 void Trainer::reserve_pool() {
-    if (const char* e = std::getenv("AH_POOL_RESERVE"))
-        if (e[0] == '0') return;
     size_t free_b = 0, total_b = 0;
     check(cudaMemGetInfo(&free_b, &total_b), "mem info");
     const int64_t transient = std::max<int64_t>(0, sim_.peak_gpu - (int64_t)static_bytes_);
@@ -836,7 +826,6 @@ void Trainer::compute_after_side() {
 // cast from the fp32 master (+ DP all-gather) — so it overlaps op idx instead of preceding the
 // next op on the compute stream. Only the compute lane thread touches these blocks' buffers.
 void Trainer::prefetch_weights(const Iter& it, size_t idx, RtOp& cur) {
-    if (!prefetch_mat_) return;
     const std::vector<OpKey>& order = it.lane_order[kCompute];
     if (idx + 1 >= order.size()) return;
     const OpKey& x = order[idx];

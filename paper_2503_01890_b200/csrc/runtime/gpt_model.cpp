@@ -72,8 +72,6 @@ GemmArgs linear_wgrad(const GptDims& d, const uint16_t* dY, int N, const uint16_
     return g;
 }
 
-bool fused_attention(const GptDims& d) { return attention_mode(d) != AttnMode::Unfused; }
-
 // Per-(head, sequence) view helpers: z1 = head, z2 = sequence.
 void heads(GemmArgs& g, const GptDims& d) {
     g.batch1 = d.nh;
@@ -82,16 +80,10 @@ void heads(GemmArgs& g, const GptDims& d) {
 
 }  // namespace
 
-// head_dim 128 and s % 128 == 0 run a fused tcgen05 kernel; AH_ATTENTION=twopass / unfused
-// select the P-saving paths (A/B checks); other shapes fall back to unfused.
+// head_dim 128 and s % 128 == 0 run the flash tcgen05 kernels; other shapes (e.g. head_dim 64)
+// take the unfused path: S GEMM, softmax kernel, P V GEMM, with P kept for the backward.
 AttnMode attention_mode(const GptDims& d) {
-    static const std::string env = [] {
-        const char* e = std::getenv("AH_ATTENTION");
-        return std::string(e ? e : "");
-    }();
-    if (env == "unfused" || !gpt::flash_supported(d.hd, d.s)) return AttnMode::Unfused;
-    if (env == "twopass" || env == "fused") return AttnMode::TwoPass;
-    return AttnMode::Flash;
+    return gpt::flash_supported(d.hd, d.s) ? AttnMode::Flash : AttnMode::Unfused;
 }
 
 namespace {
@@ -196,8 +188,6 @@ cudaError_t block_forward(const GptDims& d, const uint16_t* W, const uint16_t* x
     const AttnMode mode = attention_mode(d);
     if (mode == AttnMode::Flash) {  // one tcgen05 kernel: S, online softmax, P V; keeps O and lse
         AH_TRY(gpt::flash_fwd(a.qkv, a.att, a.lse2, d.B, s, d.nh, hd, 1.0f / std::sqrt((float)hd), st));
-    } else if (mode == AttnMode::TwoPass) {  // S, exact softmax, P (kept for the backward), P V
-        AH_TRY(gpt::attn_fwd(a.qkv, a.P, a.att, d.B, s, d.nh, hd, 1.0f / std::sqrt((float)hd), st));
     } else {
     {  // S = Q K^T / sqrt(hd), causal tiles only, fp32
         GemmArgs g;
@@ -282,11 +272,9 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
     AH_TRY(gemm::run(linear_wgrad(d, ws.dx2, h, a.att, h, W + o.w_proj), st));
     if (!ln_fused) AH_TRY(gpt::colsum(ws.dx2, T, h, h, ws.part, W + o.b_proj, 0, st));
     // ---- attention core, per (head, sequence)
-    const bool fused = fused_attention(d);
-    if (attention_mode(d) == AttnMode::Flash) {  // P recomputed from lse; dS (-> HBM for dQ), dV, dK
+    const bool fused = attention_mode(d) == AttnMode::Flash;
+    if (fused) {  // P recomputed from lse; dS^T (-> HBM for dQ), dV, dK
         AH_TRY(gpt::flash_bwd(a.qkv, a.att, ws.datt, a.lse2, ws.S, ws.dS, ws.dqkv, d.B, s, d.nh, hd, scale, st));
-    } else if (fused) {  // one tcgen05 kernel: dP, dS (-> HBM for dQ), dV, dK; D = rowsum(dO * O) in ws.S
-        AH_TRY(gpt::attn_bwd(a.qkv, a.att, ws.datt, a.P, ws.S, ws.dS, ws.dqkv, d.B, s, d.nh, hd, scale, st));
     } else {
     {  // dP = dO V^T (fp32, lower tiles)
         GemmArgs g;
@@ -315,8 +303,8 @@ cudaError_t block_backward(const GptDims& d, uint16_t* W, const uint16_t* x_in, 
         heads(g, d);
         g.M = s; g.N = hd; g.K = s;
         g.A = ws.dS; g.lda = s; g.a_s1 = (long long)s * s; g.a_s2 = (long long)d.nh * s * s;
-        // the default flash backward stores dS^T [key][query]: read it as an MN-major A
-        g.a_mn_major = attention_mode(d) == AttnMode::Flash && gpt::flash_bwd_ds_transposed() ? 1 : 0;
+        // the flash backward stores dS^T [key][query]: read it as an MN-major A
+        g.a_mn_major = fused ? 1 : 0;
         g.B = a.qkv + h; g.b_mn_major = 1; g.ldb = 3 * h; g.b_s1 = hd; g.b_s2 = (long long)s * 3 * h;
         g.C = ws.dqkv; g.ldc = 3 * h; g.c_s1 = hd; g.c_s2 = (long long)s * 3 * h;
         g.alpha = scale;

@@ -42,10 +42,10 @@ struct BlockLayout {
 
 // Saved activations of one block besides its input (the recomputable "drop" part of
 // simulator.cpp:98-102): carved from one allocation.
-// Attention implementation (process-wide, env AH_ATTENTION): flash (default: O + per-row lse
-// saved, P recomputed in the backward), twopass (fused two-pass kernel, P saved) or unfused
-// (GEMM + softmax + GEMM, P saved). It decides what a block keeps (P or lse) and the workspace.
-enum class AttnMode { Flash, TwoPass, Unfused };
+// Attention implementation, by shape: flash (head_dim 128, s % 128 == 0: O + per-row lse saved,
+// P recomputed in the backward) or unfused (GEMM + softmax + GEMM, P saved). It decides what a
+// block keeps (P or lse) and the workspace.
+enum class AttnMode { Flash, Unfused };
 AttnMode attention_mode(const GptDims& d);
 
 struct BlockActs {

@@ -1,46 +1,41 @@
-"""The fused tcgen05 attention paths (flash: O + lse saved, P recomputed; twopass: P saved) and
-the unfused GEMM + softmax + GEMM path give the same training step within bf16 tolerance (the
-path is selected with AH_ATTENTION in a subprocess, since the choice is latched per process)."""
-import json
-import os
-import subprocess
-import sys
-
+"""The unfused attention path (S GEMM + softmax kernel + P V GEMM, P kept), taken for shapes the
+flash kernels do not cover (head_dim != 128), trains the same step as a torch fp32 reference.
+The flash path is checked the same way in test_trainer_gpu.py / test_baseline_shapes_gpu.py."""
 import numpy as np
 import pytest
+import torch
 
-from tests.conftest import ROOT
+from tests import gpt_reference as ref
 
 pytestmark = pytest.mark.gpu
 
-SCRIPT = r"""
-import json, sys, numpy as np
-sys.path.insert(0, %r)
-from paper_2503_01890_b200.trainer import AdamConfig, ModelConfig, PlanConfig, Trainer
-m = ModelConfig(num_blocks=2, hidden=256, heads=2, seq_len=512, batch=2, vocab=1000)
-tr = Trainer(m, PlanConfig(c_hat=1, p_hat=0, o_hat=0, fine_tune=False, gpu_mem_budget=1 << 40),
-             AdamConfig(lr=1.0, eps=1.0, weight_decay=0.0), seed=5, cpu_threads=2)
-rng = np.random.default_rng(1)
-t = rng.integers(0, m.vocab, size=m.batch * m.seq_len, dtype=np.int32)
-y = rng.integers(0, m.vocab, size=m.batch * m.seq_len, dtype=np.int32)
-before = [tr.master(i).copy() for i in (1, 2)]
-loss = tr.step(t, y)
-delta = [(tr.master(i) - b).tolist() for i, b in zip((1, 2), before)]
-print(json.dumps({"loss": loss, "delta": delta}))
-"""
 
-
-def run(env_extra):
-    env = dict(os.environ, **env_extra)
-    out = subprocess.run([sys.executable, "-c", SCRIPT % ROOT], env=env, capture_output=True, text=True, check=True)
-    return json.loads(out.stdout.strip().splitlines()[-1])
-
-
-@pytest.mark.parametrize("mode", ["flash", "twopass"])
-def test_fused_and_unfused_attention_agree(cuda_device, native, mode):
-    fused = run({"AH_ATTENTION": mode})
-    unfused = run({"AH_ATTENTION": "unfused"})
-    assert abs(fused["loss"] - unfused["loss"]) < 1e-3 * abs(unfused["loss"])
-    for a, b in zip(fused["delta"], unfused["delta"]):
-        a, b = np.array(a), np.array(b)
-        assert np.linalg.norm(a - b) / np.linalg.norm(b) < 3e-2
+@pytest.mark.parametrize("heads", [4, 8])  # head_dim 64, 32
+def test_unfused_path_matches_torch(cuda_device, native, heads):
+    from paper_2503_01890_b200.trainer import AdamConfig, ModelConfig, PlanConfig, Trainer
+    model = ModelConfig(num_blocks=2, hidden=256, heads=heads, seq_len=256, batch=2, vocab=1000)
+    if heads == 8:  # the trainer needs head_dim % 64 == 0
+        with pytest.raises(Exception):
+            Trainer(model, PlanConfig(c_hat=0, p_hat=0, o_hat=0, fine_tune=False, gpu_mem_budget=1 << 40))
+        return
+    lr = 1e3
+    tr = Trainer(model, PlanConfig(c_hat=1, p_hat=0, o_hat=1, fine_tune=False, gpu_mem_budget=1 << 40),
+                 AdamConfig(lr=lr, eps=1.0, weight_decay=0.0), seed=5, cpu_threads=2)
+    h = model.hidden
+    before = [torch.from_numpy(tr.master(i).copy()) for i in (1, 2)]
+    wte = torch.from_numpy(tr.master(0).copy()).view(-1, h)
+    wpe = torch.from_numpy(tr.master(-1).copy()).view(-1, h)
+    lnf = torch.from_numpy(tr.master(-2).copy())
+    rng = np.random.default_rng(1)
+    t = rng.integers(0, model.vocab, size=(model.batch, model.seq_len), dtype=np.int32)
+    y = rng.integers(0, model.vocab, size=(model.batch, model.seq_len), dtype=np.int32)
+    loss = tr.step(t, y)
+    after = [torch.from_numpy(tr.master(i).copy()) for i in (1, 2)]
+    tr.close()
+    rl, g_blocks, _, _, _ = ref.loss_and_grads(before, wte, wpe, lnf, torch.from_numpy(t).long(),
+                                               torch.from_numpy(y).long(), heads, model.vocab)
+    assert abs(loss - rl) / rl < 1e-2
+    for i in range(2):
+        est = -(after[i] - before[i]) / lr
+        exp = g_blocks[i].reshape(-1) / (g_blocks[i].reshape(-1).abs() + 1.0)
+        assert float((est - exp).norm() / exp.norm()) < 5e-2, i
