@@ -221,6 +221,10 @@ int ah_dp_unique_id(uint8_t* out);
  * collective semantics as the NCCL path; device copies + a fixed-order sum kernel). */
 int ah_dp_loopback_create(int32_t nranks, void** comm);
 int ah_dp_loopback_destroy(void* comm);
+/* One rank's side of a loopback collective (blocks until every rank has posted it): op 0 =
+ * all-gather bf16 (count = shard), 1 = reduce-scatter bf16 sum (count = shard), 2 = all-reduce
+ * fp32, 3 = all-reduce bf16 (count = elements). buf = this rank's full buffer, in place. */
+int ah_dp_loopback_call(void* comm, int32_t rank, int32_t op, void* buf, size_t count, void* stream);
 int ah_dp_shard(int64_t n, int32_t rank, int32_t dp_size, int64_t* offset, int64_t* len, int64_t* shard);
 
 /* ---------------------------------------------------------------------------------------

@@ -196,6 +196,7 @@ _EXTRA_SIGS.update({
     "ah_dp_unique_id": ([C.c_void_p], C.c_int),
     "ah_dp_loopback_create": ([C.c_int32, C.POINTER(C.c_void_p)], C.c_int),
     "ah_dp_loopback_destroy": ([C.c_void_p], C.c_int),
+    "ah_dp_loopback_call": ([C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_size_t, C.c_void_p], C.c_int),
     "ah_dp_shard": ([C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                      C.POINTER(C.c_int64)], C.c_int),
 })

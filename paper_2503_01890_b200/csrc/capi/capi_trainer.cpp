@@ -175,6 +175,13 @@ int ah_dp_loopback_create(int32_t nranks, void** comm) {
     return AH_OK;
 }
 
+int ah_dp_loopback_call(void* comm, int32_t rank, int32_t op, void* buf, size_t count, void* stream) {
+    if (!comm || !buf || op < 0 || op > 3) return ah::set_error(AH_ERR_INVALID, "ah_dp_loopback_call: bad argument");
+    return ah::cuda_status(static_cast<ah::LoopbackComm*>(comm)->call(rank, static_cast<ah::LoopbackComm::Op>(op), buf,
+                                                                      count, static_cast<cudaStream_t>(stream)),
+                           "ah_dp_loopback_call");
+}
+
 int ah_dp_loopback_destroy(void* comm) {
     delete static_cast<ah::LoopbackComm*>(comm);
     return AH_OK;

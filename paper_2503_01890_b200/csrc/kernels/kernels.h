@@ -22,8 +22,10 @@ struct AdamArgs {
 };
 
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);
-// dst[i] = sum over q < n (in order) of srcs[q][i], fp32 accumulation (loopback collectives).
-cudaError_t launch_sum_ranks(void* dst, const void* const* srcs, int n, size_t count, bool f32, cudaStream_t st);
+// dst[i] = sum over q < n (in order) of srcs[q][i] (loopback collectives): fp32 accumulation, or
+// (ring, bf16) NCCL ring's per-hop bf16 rounding of the running partial.
+cudaError_t launch_sum_ranks(void* dst, const void* const* srcs, int n, size_t count, bool f32, cudaStream_t st,
+                             bool ring = false);
 cudaError_t launch_cast_f32_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t stream);
 cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, float* stats,
                               cudaStream_t stream);

@@ -38,12 +38,16 @@ cudaError_t LoopbackComm::perform(Slot& s) {
                                             static_cast<uint16_t*>(s.posts[(size_t)r].buf) + (size_t)r * c, c * 2,
                                             cudaMemcpyDeviceToDevice, stream_);
             break;
-        case kReduceScatterBf16: {  // chunk r of every rank, summed in rank order -> rank r's chunk r
+        case kReduceScatterBf16: {  // chunk r, NCCL ring order: starts at rank r+1, hops r+2 .. r-1,
+            // ends at its owner r; each hop rounds the running partial to bf16 -> rank r's chunk r
             for (int r = 0; r < n_ && e == cudaSuccess; ++r) {
                 const void* src[8];
-                for (int q = 0; q < n_; ++q) src[q] = static_cast<uint16_t*>(s.posts[(size_t)q].buf) + (size_t)r * c;
+                for (int k = 0; k < n_; ++k) {
+                    const int q = (r + 1 + k) % n_;
+                    src[k] = static_cast<uint16_t*>(s.posts[(size_t)q].buf) + (size_t)r * c;
+                }
                 e = launch_sum_ranks(static_cast<uint16_t*>(s.posts[(size_t)r].buf) + (size_t)r * c, src, n_, c, false,
-                                     stream_);
+                                     stream_, /*ring=*/true);
             }
             break;
         }

@@ -4,7 +4,9 @@
 // parallel path — shard offsets, 1/N gradient scaling, replicated-embedding all-reduce and the
 // side-stream ordering of every collective — can be executed end to end on a single-GPU box
 // (NCCL refuses two ranks on one device). Not a transport: everything is device memcpy / a
-// fixed-order sum kernel on one internal stream.
+// fixed-order sum kernel on one internal stream. The bf16 reduce-scatter reproduces NCCL's ring
+// algorithm (chunk r accumulated from rank r+1 around the ring to r, bf16 rounding per hop); the
+// all-reduces accumulate in fp32 and round once.
 //
 // Rendezvous: each rank numbers its collective calls; call k blocks the calling host thread
 // until every rank has posted call k (with an event marking its inputs ready on its stream);

@@ -92,3 +92,51 @@ def test_dp_loopback_is_deterministic(cuda_device, native):
     assert l1 == l2
     for a, b in zip(b1, b2):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+@pytest.mark.parametrize("n", [2, 3, 8])
+def test_loopback_reduce_scatter_is_nccl_ring(cuda_device, native, n):
+    """The loopback bf16 reduce-scatter computes exactly NCCL's ring algorithm (chunk r summed from
+    rank r+1 around the ring to its owner r, rounding the running partial to bf16 at every hop),
+    and the dp-n tolerance derived for it holds: |ring - exact| <= (n-1) * 2^-8 * sum_q |g_q|
+    per element (bf16 unit roundoff 2^-8, one rounding per hop)."""
+    import threading
+
+    import torch
+
+    from oracle import adam as oadam
+    from paper_2503_01890_b200 import _native as N
+    from paper_2503_01890_b200.trainer import LoopbackComm
+    shard = 100_003
+    g = torch.Generator(device="cuda").manual_seed(n)
+    # mixed magnitudes so the per-hop rounding matters
+    bufs = [(torch.randn(n * shard, device="cuda", generator=g) * torch.exp(
+        torch.randn(n * shard, device="cuda", generator=g) * 2)).bfloat16() for _ in range(n)]
+    host = [b.view(torch.int16).cpu().numpy().view(np.uint16) for b in bufs]
+    torch.cuda.synchronize()
+    comm = LoopbackComm(n)
+    errs = []
+
+    def rank(r):
+        rc = N.lib().ah_dp_loopback_call(comm.handle, r, 1, bufs[r].data_ptr(), shard, None)
+        errs.append(rc)
+
+    ts = [threading.Thread(target=rank, args=(r,)) for r in range(n)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    torch.cuda.synchronize()
+    comm.close()
+    assert errs == [0] * n
+    for r in range(n):
+        sl = slice(r * shard, (r + 1) * shard)
+        acc = oadam.bf16_bits_to_f32(host[(r + 1) % n][sl])
+        for k in range(1, n):
+            acc = oadam.bf16_bits_to_f32(oadam.cast_bf16(acc + oadam.bf16_bits_to_f32(host[(r + 1 + k) % n][sl])))
+        got = bufs[r].view(torch.int16).cpu().numpy().view(np.uint16)[sl]
+        assert np.array_equal(got, oadam.cast_bf16(acc)), r
+        vals = np.stack([oadam.bf16_bits_to_f32(h[sl]).astype(np.float64) for h in host])
+        exact, mag = vals.sum(0), np.abs(vals).sum(0)
+        err = np.abs(oadam.bf16_bits_to_f32(got).astype(np.float64) - exact)
+        assert np.all(err <= (n - 1) * 2.0 ** -8 * mag + 1e-30), r
