@@ -374,6 +374,7 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
     st_t = tr.stats()  # lanes over the timed region; offload window = its last iterations
     loss = tr.drain()
     _, mem_peak = tr.memory_csv()  # measured timeline of the window (reference CSV schema)
+    cal = tr.calibrate()  # the window's in-step block durations in the reference cost model
     value = T * steps * world / (ms_max / 1e3)
 
     # ---- GEMM window: CUDA events around every GEMM launch (an event between two kernels costs
@@ -476,6 +477,15 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
                                                            st_t["sim_lane_busy_ms"])),
                          "note": "simulated = reference scheduler durations from the measured rates "
                                  "(steady-state iteration of hetsim::run)"},
+        "calibration": {"in_step_block_s": {k: cal[k] for k in ("t_fwd_s", "t_bwd_s", "t_recompute_s", "t_h2d_s",
+                                                                  "t_d2h_s", "t_opt_cpu_s", "t_opt_gpu_s")},
+                        "sim_steady_ms": cal["sim_steady_s"] * 1e3,
+                        "measured_over_sim": per / (cal["sim_steady_s"] * 1e3) if cal["sim_steady_s"] > 0 else None,
+                        "replan_strategy": [cal["c_hat"], cal["p_hat"], cal["o_hat"]],
+                        "replan_sim_steady_ms": cal["sim_steady_replan_s"] * 1e3,
+                        "note": "the running plan re-simulated by the reference scheduler with the block durations "
+                                "measured inside the timed window (profiler fidelity); replan = hetsim::solve with "
+                                "them"},
         "memory": {"measured_peak_gib": mem_peak / 2**30, "simulated_peak_gib": st["simulated_peak_bytes"] / 2**30,
                    "eq1_gib": st["modeled_peak_bytes"] / 2**30,
                    "source": "Trainer.memory_csv(): persistent + stream-ordered transient buffers at op start / end"},
@@ -581,8 +591,8 @@ def main():
                           "tens of GB >> 126 MB L2"),
     }
     for k in ("e2e", "gpu_launches", "roofline", "model_flops_per_token", "mfu_model", "loss", "bound_by",
-              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "lanes_vs_sim", "memory", "ps_gain", "grad",
-              "profiled_rates", "clocks", "init_s"):
+              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "lanes_vs_sim", "calibration", "memory",
+              "ps_gain", "grad", "profiled_rates", "clocks", "init_s"):
         line[k] = head[k]
     if dist:
         line["nccl_ranks"] = dist.get_world_size()
@@ -609,8 +619,8 @@ def main():
             r = run_workload(a, name, GPU_BUDGET_GIB[name], a.steps, a.warmup, rank, world, local, None,
                              headline=False)
             sec[name] = {k: r[k] for k in ("value", "ms_per_step", "e2e", "roofline", "mfu_model", "bound_by",
-                                           "lane_busy_ms_per_step", "lanes_vs_sim", "memory", "plan", "offload",
-                                           "ps_gain", "grad", "clocks")}
+                                           "lane_busy_ms_per_step", "lanes_vs_sim", "calibration", "memory", "plan",
+                                           "offload", "ps_gain", "grad", "clocks")}
             sec[name]["workload"] = workload_config(argparse.Namespace(config=name, strategy="",
                                                                        gpu_mem_gib=GPU_BUDGET_GIB[name]),
                                                     CONFIGS[name], 1)["workload"]

@@ -342,6 +342,22 @@ typedef struct ah_hw_profile {
 } ah_hw_profile;
 int ah_profile_block(const ah_trainer_config* cfg, ah_hw_profile* out);
 
+/* In-step calibration (profiler fidelity): the per-block durations the running trainer actually
+ * achieved over its last drained iterations — means over the window of F, B, GpuOptim ops
+ * (CUDA events; F / B include the 1/L share of embedding / head work the blocks carry),
+ * ParamPrefetch / GradOffload copies of optimizer-offloaded blocks, and CpuOptim (host clock) —
+ * put into the reference cost model: sim_steady_s = hetsim::run of the running plan with them;
+ * (c_hat, p_hat, o_hat) = the plan hetsim::solve (+ fine_tune_prefetch) picks with them
+ * (single-GPU trainers; -1 under DP) and sim_steady_replan_s its simulated iteration. */
+typedef struct ah_calibration {
+    double t_fwd_s, t_bwd_s, t_recompute_s;   /* per block (0 if no op of that kind ran) */
+    double t_h2d_s, t_d2h_s, t_opt_cpu_s, t_opt_gpu_s;
+    double sim_steady_s;
+    int32_t c_hat, p_hat, o_hat;
+    double sim_steady_replan_s;
+} ah_calibration;
+int ah_trainer_calibrate(void* trainer, ah_calibration* out);
+
 /* Host side of the profiler: the CpuOptim lane's roofline on this host. n params of pinned
  * 14 B/param state (allocated and freed inside: a setup call); stream_gbps = best in-place pass
  * over p/m/v (fp32) and g (bf16) with trivial arithmetic (the 28 B/param pattern of the host

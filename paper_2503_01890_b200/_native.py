@@ -182,7 +182,15 @@ class HostProfile(C.Structure):
                 ("threads", C.c_int32)]
 
 
+class Calibration(C.Structure):
+    _fields_ = [("t_fwd_s", C.c_double), ("t_bwd_s", C.c_double), ("t_recompute_s", C.c_double),
+                ("t_h2d_s", C.c_double), ("t_d2h_s", C.c_double), ("t_opt_cpu_s", C.c_double),
+                ("t_opt_gpu_s", C.c_double), ("sim_steady_s", C.c_double), ("c_hat", C.c_int32),
+                ("p_hat", C.c_int32), ("o_hat", C.c_int32), ("sim_steady_replan_s", C.c_double)]
+
+
 _EXTRA_SIGS.update({
+    "ah_trainer_calibrate": ([C.c_void_p, C.POINTER(Calibration)], C.c_int),
     "ah_trainer_set_schedule": ([C.c_void_p, C.c_int32], C.c_int),
     "ah_trainer_memory_csv": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)], C.c_int),
     "ah_profile_host": ([C.c_size_t, C.c_int32, C.POINTER(HostProfile)], C.c_int),

@@ -28,6 +28,7 @@ int set_error(int code, const std::string& msg) {
 
 int cuda_status(cudaError_t e, const char* where) {
     if (e == cudaSuccess) return AH_OK;
+    cudaGetLastError();  // reported here: do not let it resurface at the next launch check
     return set_error(AH_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 }  // namespace ah

@@ -13,21 +13,23 @@ namespace {
 
 template <class F>
 int guarded(F&& f) {
+    int rc = AH_OK;
     try {
         f();
-        return AH_OK;
     } catch (const hetsim::InfeasibleError& e) {
-        return ah::set_error(AH_ERR_INFEASIBLE, e.what());
+        rc = ah::set_error(AH_ERR_INFEASIBLE, e.what());
     } catch (const hetsim::MemoryExceededError& e) {
-        return ah::set_error(AH_ERR_MEMORY, e.what());
+        rc = ah::set_error(AH_ERR_MEMORY, e.what());
     } catch (const std::invalid_argument& e) {
-        return ah::set_error(AH_ERR_INVALID, e.what());
+        rc = ah::set_error(AH_ERR_INVALID, e.what());
     } catch (const std::exception& e) {
         const std::string w = e.what();
-        return ah::set_error(w.find("CUDA") != std::string::npos || w.find("cuda") != std::string::npos ? AH_ERR_CUDA
-                                                                                                         : AH_ERR_INTERNAL,
-                             w);
+        rc = ah::set_error(w.find("CUDA") != std::string::npos || w.find("cuda") != std::string::npos ? AH_ERR_CUDA
+                                                                                                       : AH_ERR_INTERNAL,
+                           w);
     }
+    if (rc != AH_OK) cudaGetLastError();  // reported here; keep it out of later launch checks
+    return rc;
 }
 
 ah::Trainer* T(void* p) { return static_cast<ah::Trainer*>(p); }
@@ -82,6 +84,11 @@ int ah_trainer_stats_get(void* tr, ah_trainer_stats* out) {
 int ah_trainer_reset_stats(void* tr) {
     if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
     return guarded([&] { T(tr)->reset_stats(); });
+}
+
+int ah_trainer_calibrate(void* tr, ah_calibration* out) {
+    if (!tr || !out) return ah::set_error(AH_ERR_INVALID, "ah_trainer_calibrate: null argument");
+    return guarded([&] { T(tr)->calibrate(out); });
 }
 
 int ah_trainer_set_schedule(void* tr, int32_t priority_sched) {

@@ -205,6 +205,10 @@ void Trainer::plan(const ah_trainer_config& cfg) {
     m_gc += (size_t)(d_.L + 1) * T * h * 2 + 2 * T * h * 2 + Workspace::bytes(d_);
     hetsim::ProfileOverrides ov;
     ov.m_gc = (std::int64_t)m_gc;
+    spec_ = spec;
+    ov_ = ov;
+    hw_cfg_ = hw_;
+    fine_tune_ = cfg.fine_tune != 0;
     profile_ = hetsim::build_profile(spec, hw_, ov);
     const int L = d_.L;
     if (cfg.c_hat >= 0 && cfg.p_hat >= 0 && cfg.o_hat >= 0) {
@@ -250,6 +254,85 @@ void Trainer::compile_order() {
         if (op.iter > 2) continue;
         order_[op.iter - 1][lane_of(op.kind)].push_back({(int)op.kind, op.block, op.backward_copy});
         if (op.iter == 2) sim_lane_ms_[lane_of(op.kind)] += (op.end - op.start) * 1e3;
+    }
+}
+
+void Trainer::calibrate(ah_calibration* out) {
+    drain();
+    std::memset(out, 0, sizeof(*out));
+    double sum[7] = {0}, cnt[7] = {0};  // F, B, R, H2D, D2H, CPU, GPU-opt
+    {
+        std::lock_guard<std::mutex> lk(mu_);
+        for (Iter* it : iters_)
+            for (auto& kv : it->ops) {
+                const RtOp& o = kv.second;
+                int k = -1;
+                switch (o.kind) {
+                    case OpKind::Forward: k = 0; break;
+                    case OpKind::Backward: k = 1; break;
+                    case OpKind::Recompute: k = 2; break;
+                    case OpKind::ParamPrefetch: k = blocks_[(size_t)o.block].o ? 3 : -1; break;  // PCIe copies only
+                    case OpKind::GradOffload: k = 4; break;
+                    case OpKind::CpuOptim: k = 5; break;
+                    case OpKind::GpuOptim: k = 6; break;
+                    default: break;
+                }
+                if (k < 0) continue;
+                double ms = o.host_ms;
+                if (o.lane != kCpu) {
+                    float x = 0.f;
+                    if (cudaEventElapsedTime(&x, o.t0, o.t1) != cudaSuccess) continue;
+                    ms = x;
+                }
+                sum[k] += ms / 1e3;
+                cnt[k] += 1;
+            }
+    }
+    auto mean = [&](int k) { return cnt[k] > 0 ? sum[k] / cnt[k] : 0.0; };
+    out->t_fwd_s = mean(0);
+    out->t_bwd_s = mean(1);
+    out->t_recompute_s = mean(2);
+    out->t_h2d_s = mean(3);
+    out->t_d2h_s = mean(4);
+    out->t_opt_cpu_s = mean(5);
+    out->t_opt_gpu_s = mean(6);
+    // the running plan in the reference cost model with the measured durations
+    hetsim::ModelProfile cal = profile_;
+    hetsim::BlockProfile& b = cal.block;
+    if (cnt[0] > 0) b.t_fp = out->t_fwd_s;
+    if (cnt[1] > 0) b.t_bp = out->t_bwd_s;
+    if (cnt[3] > 0) b.t_h2d = out->t_h2d_s;
+    if (cnt[4] > 0) b.t_d2h = out->t_d2h_s;
+    if (cnt[5] > 0) b.t_opt_cpu = out->t_opt_cpu_s;
+    if (cnt[6] > 0) b.t_opt_gpu = out->t_opt_gpu_s;
+    out->sim_steady_s = hetsim::run(cal, strategy_, hw_, 3, ps_).steady_state_time;
+    out->c_hat = out->p_hat = out->o_hat = -1;
+    if (dp_size_ > 1) return;
+    // the plan the reference planner picks with these durations expressed as HardwareSpec rates
+    // (the inverse of estimate_block_times, workload.cpp:55-73)
+    hetsim::HardwareSpec hw = hw_cfg_;
+    hetsim::ModelSpec spec = spec_;
+    const double mp = (double)profile_.block.m_p;
+    const double flops = 2.0 * mp * (double)d_.T() + 4.0 * d_.B * (double)d_.s * d_.s * d_.h;
+    hw.gpu_compute_rate = flops / b.t_fp;
+    spec.bwd_fwd_ratio = b.t_bp / b.t_fp;
+    hw.h2d_bandwidth = 2.0 * mp / b.t_h2d;
+    hw.d2h_bandwidth = 2.0 * mp / b.t_d2h;
+    hw.cpu_optim_rate = mp / b.t_opt_cpu;
+    hw.gpu_optim_rate = mp / b.t_opt_gpu;
+    try {
+        const hetsim::ModelProfile pr = hetsim::build_profile(spec, hw, ov_);
+        hetsim::PlanRequest req;
+        req.profile = pr;
+        req.hardware = hw;
+        hetsim::Strategy st = hetsim::solve(req).strategy;
+        if (fine_tune_) st = hetsim::fine_tune_prefetch(pr, st, hw);
+        out->c_hat = st.c_hat;
+        out->p_hat = st.p_hat;
+        out->o_hat = st.o_hat;
+        out->sim_steady_replan_s = hetsim::run(pr, st, hw, 3, ps_).steady_state_time;
+    } catch (const std::exception&) {
+        // infeasible with these rates: report no plan
     }
 }
 

@@ -53,6 +53,8 @@ public:
     // Switch the per-lane order of subsequent iterations between the priority-based (paper §3.3)
     // and the FIFO schedule of the reference scheduler (drains first; weights / state kept).
     void set_schedule(bool priority);
+    // In-step calibration of the block durations from the drained window (ah_calibration).
+    void calibrate(ah_calibration* out);
     void stats(ah_trainer_stats* out);
     void reset_stats();  // zero the lane busy-time counters and the offload window
     // fp32 master of block b (1-based; 0 = embedding wte, -1 = wpe, -2 = final LN) -> host.
@@ -164,6 +166,10 @@ private:
     hetsim::HardwareSpec hw_;
     hetsim::Strategy strategy_;
     hetsim::dp::DpSpec dp_spec_;
+    hetsim::ModelSpec spec_;            // model as given to build_profile
+    hetsim::ProfileOverrides ov_;       // m_gc of this runtime
+    hetsim::HardwareSpec hw_cfg_;       // rates / budgets as configured (before DP adjustments)
+    bool fine_tune_ = false;
     hetsim::SimResult sim_;
     double sim_steady_[2] = {0.0, 0.0};  // reference scheduler steady state: [0] FIFO, [1] PS
     double sim_lane_ms_[4] = {0, 0, 0, 0};  // simulated busy time per lane, steady iteration

@@ -147,6 +147,13 @@ class Trainer:
     def reset_stats(self) -> None:
         N.check(N.lib().ah_trainer_reset_stats(self._h), "ah_trainer_reset_stats")
 
+    def calibrate(self) -> dict:
+        """In-step block durations of the drained window, the running plan's simulated iteration
+        with them, and the plan the reference planner would pick with them."""
+        out = N.Calibration()
+        N.check(N.lib().ah_trainer_calibrate(self._h, C.byref(out)), "ah_trainer_calibrate")
+        return {f: getattr(out, f) for f, _ in out._fields_}
+
     def set_schedule(self, priority: bool) -> None:
         """Priority-based (True) or FIFO (False) per-lane order for the following iterations."""
         N.check(N.lib().ah_trainer_set_schedule(self._h, int(priority)), "ah_trainer_set_schedule")

@@ -282,3 +282,20 @@ def test_profile_block(cuda_device, native):
     host = profile_host(20_000_000, 4)
     assert host["stream_gbps"] > 0 and host["adam_gbps"] > 0
     assert p["cpu_adam_rate"] * 28 / 1e9 < 1.5 * host["stream_gbps"]
+
+
+def test_calibrate_from_window(cuda_device, native):
+    """In-step calibration: every op kind the plan runs has a positive mean duration, and the
+    running plan re-simulated with them is a positive iteration time; the replan is valid."""
+    from paper_2503_01890_b200.trainer import PlanConfig
+    tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=2, fine_tune=False, gpu_mem_budget=1 << 40))
+    for k in range(4):
+        tr.submit(*batch(k))
+    tr.drain()
+    c = tr.calibrate()
+    tr.close()
+    for k in ("t_fwd_s", "t_bwd_s", "t_recompute_s", "t_h2d_s", "t_d2h_s", "t_opt_cpu_s", "t_opt_gpu_s",
+              "sim_steady_s", "sim_steady_replan_s"):
+        assert c[k] > 0, k
+    L = MODEL["num_blocks"]
+    assert 0 <= c["p_hat"] <= c["o_hat"] <= L and 0 <= c["c_hat"] <= L
