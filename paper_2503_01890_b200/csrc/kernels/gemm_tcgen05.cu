@@ -249,12 +249,22 @@ __device__ __forceinline__ Tile decode(const Params& P, int ct, int BN, int cran
         const int z = rest / P.tiles_n;
         return decode_at(P, z, tm, rest - z * P.tiles_n, BN);
     }
+    // Grouped raster: bands of kBand cluster-tile rows, each band walked N column by N column
+    // (rows fastest), so the ~74 tiles in flight cover kBand M rows x ~9 N columns: the A band
+    // (kBand x 256 rows) stays in L2 while B streams once per band. Row-major order (N fastest)
+    // put a whole M row in flight and re-read B from DRAM once per M row when B > L2 (the
+    // 10B / 20B qkv, fc, fc2 and LM-head shapes: 226 MB of B x 32 M rows for qkv at h = 6144).
+    constexpr int kBand = 16;
     const int tmg = (P.tiles_m + CS - 1) / CS;
     const int per_z = tmg * P.tiles_n;
     const int z = ct / per_z;
     const int rem = ct - z * per_z;
-    const int g = rem / P.tiles_n;
-    return decode_at(P, z, g * CS + crank, rem - g * P.tiles_n, BN);
+    const int band = rem / (kBand * P.tiles_n);
+    const int rows = tmg - band * kBand < kBand ? tmg - band * kBand : kBand;
+    const int r2 = rem - band * kBand * P.tiles_n;
+    const int tn = r2 / rows;
+    const int g = band * kBand + (r2 - tn * rows);
+    return decode_at(P, z, g * CS + crank, tn, BN);
 }
 
 // ---- work assignment -------------------------------------------------------------------
