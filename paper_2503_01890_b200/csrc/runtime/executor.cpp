@@ -772,10 +772,11 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
             check(block_forward(d_, b.wbuf, x_[(size_t)i - 1], x_[(size_t)i], a, ws_, st), "block fwd");
             if (i == d_.L) head_forward_backward(it);
             if (b.c) free_acts();
-            // P blocks re-fetch for the backward; GPU-resident masters re-materialise by a cast —
-            // except under DP, where that would be a second all-gather: non-P weights stay live
-            // from F to B (Eq. 1 counts them resident: 2 m_p (L - p_hat + 1), costmodel.cpp:36-41)
-            if (b.p || (!b.o && !dp_)) free_wbuf();
+            // P blocks re-fetch their weights for the backward; every other block keeps its bf16
+            // weights live from F to R / B, as Eq. 1 models them (2 m_p (L - p_hat + 1) resident,
+            // costmodel.cpp:36-41): no second cast from the master (and, under DP, no second
+            // all-gather) per iteration
+            if (b.p) free_wbuf();
             break;
         }
         case OpKind::Recompute: {
