@@ -406,13 +406,18 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
             tr.drain()
             res[ps] = timed(kp) / kp
         st_ps = tr.stats()
+        cal_ps = tr.calibrate()  # the PS window's in-step durations: the gain the model predicts with them
         sim_gain = st_ps["sim_steady_fifo_s"] / st_ps["sim_steady_ps_s"] if st_ps["sim_steady_ps_s"] > 0 else None
         ps_gain = {"measured": res[False] / res[True], "simulated": sim_gain,
+                   "simulated_calibrated": (cal_ps["sim_steady_other_s"] / cal_ps["sim_steady_s"]
+                                            if cal_ps["sim_steady_s"] > 0 else None),
                    "ms_per_step_ps": res[True], "ms_per_step_fifo": res[False],
                    "sim_steady_ms_ps": st_ps["sim_steady_ps_s"] * 1e3,
                    "sim_steady_ms_fifo": st_ps["sim_steady_fifo_s"] * 1e3, "steps_each": kp,
                    "method": "same trainer, reference scheduler order switched FIFO -> PS (set_schedule), "
-                             "2 untimed iterations after each switch, CUDA-event timed"}
+                             "2 untimed iterations after each switch, CUDA-event timed; simulated = reference "
+                             "scheduler on the profiled rates, simulated_calibrated = on the block durations "
+                             "measured in the PS window"}
     st = tr.stats()
     tr.close()
     del tr

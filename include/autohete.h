@@ -355,6 +355,7 @@ typedef struct ah_calibration {
     double sim_steady_s;
     int32_t c_hat, p_hat, o_hat;
     double sim_steady_replan_s;
+    double sim_steady_other_s; /* the running plan in the OTHER order (FIFO if PS runs, PS if FIFO) */
 } ah_calibration;
 int ah_trainer_calibrate(void* trainer, ah_calibration* out);
 

@@ -186,7 +186,8 @@ class Calibration(C.Structure):
     _fields_ = [("t_fwd_s", C.c_double), ("t_bwd_s", C.c_double), ("t_recompute_s", C.c_double),
                 ("t_h2d_s", C.c_double), ("t_d2h_s", C.c_double), ("t_opt_cpu_s", C.c_double),
                 ("t_opt_gpu_s", C.c_double), ("sim_steady_s", C.c_double), ("c_hat", C.c_int32),
-                ("p_hat", C.c_int32), ("o_hat", C.c_int32), ("sim_steady_replan_s", C.c_double)]
+                ("p_hat", C.c_int32), ("o_hat", C.c_int32), ("sim_steady_replan_s", C.c_double),
+                ("sim_steady_other_s", C.c_double)]
 
 
 _EXTRA_SIGS.update({

@@ -306,6 +306,11 @@ void Trainer::calibrate(ah_calibration* out) {
     if (cnt[5] > 0) b.t_opt_cpu = out->t_opt_cpu_s;
     if (cnt[6] > 0) b.t_opt_gpu = out->t_opt_gpu_s;
     out->sim_steady_s = hetsim::run(cal, strategy_, hw_, 3, ps_).steady_state_time;
+    try {
+        out->sim_steady_other_s = hetsim::run(cal, strategy_, hw_, 3, !ps_).steady_state_time;
+    } catch (const std::exception&) {
+        out->sim_steady_other_s = std::nan("");
+    }
     out->c_hat = out->p_hat = out->o_hat = -1;
     if (dp_size_ > 1) return;
     // the plan the reference planner picks with these durations expressed as HardwareSpec rates
