@@ -358,9 +358,39 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    for i in range(warmup):
-        tr.submit(dev_tok[i % n_batches], dev_tgt[i % n_batches])
-    tr.drain()
+    def warm(k):
+        for i in range(k):
+            tr.submit(dev_tok[i % n_batches], dev_tgt[i % n_batches])
+        tr.drain()
+
+    warm(warmup)
+    # Two-phase planning (single GPU): the isolated one-block profile plans the first trainer; the
+    # warm-up window's in-step block durations (ah_trainer_calibrate) then re-enter the planner. The
+    # same (c, p, o) -> the trainer adopts the calibrated profile / lookaheads / order in place; a
+    # different plan -> a new trainer built from the calibrated rates.
+    st0 = tr.stats()
+    planning = {"profiled_plan": [st0["c_hat"], st0["p_hat"], st0["o_hat"]],
+                "profiled_sim_steady_ms": st0["sim_steady_ps_s"] * 1e3, "calibrated": False}
+    if a.calibrate_plan and not dist:
+        cal0 = tr.calibrate()
+        keep = bool(kw)  # forced strategies keep (c, p, o)
+        if tr.apply_calibration(keep_strategy=keep):
+            planning.update(calibrated=True, rebuilt=False)
+        elif cal0["c_hat"] >= 0:
+            tr.close()
+            rates = dict(prof, gpu_flops=cal0["gpu_flops"], bwd_fwd_ratio=cal0["bwd_fwd_ratio"], h2d_bw=cal0["h2d_bw"],
+                         d2h_bw=cal0["d2h_bw"], cpu_adam_rate=cal0["cpu_adam_rate"],
+                         gpu_adam_rate=cal0["gpu_adam_rate"])
+            plan = plan_from_profile(rates, budget_gib << 30, a.cpu_mem_gib << 30)
+            tr = Trainer(model, plan, seed=1234, cpu_threads=a.cpu_threads, dp_rank=rank, dp_size=world)
+            planning.update(calibrated=True, rebuilt=True)
+            warm(warmup)
+        st1 = tr.stats()
+        planning.update(plan=[st1["c_hat"], st1["p_hat"], st1["o_hat"]],
+                        calibrated_sim_steady_ms=st1["sim_steady_ps_s"] * 1e3,
+                        rates={k: cal0[k] for k in ("gpu_flops", "bwd_fwd_ratio", "h2d_bw", "d2h_bw", "cpu_adam_rate",
+                                                    "gpu_adam_rate")})
+        warm(2)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
@@ -474,9 +504,13 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
                  "pool_peak_gib": st["pool_peak_bytes"] / 2**30, "static_gib": st["static_bytes"] / 2**30,
                  "sim_steady_ms": st["sim_steady_ps_s"] * 1e3, "measured_over_sim": per / (st["sim_steady_ps_s"] * 1e3)
                  if st["sim_steady_ps_s"] > 0 else None,
+                 "measured_over_profiled_sim": per / planning["profiled_sim_steady_ms"]
+                 if planning["profiled_sim_steady_ms"] > 0 else None,
+                 "sim_basis": "calibrated in-step rates" if planning["calibrated"] else "isolated one-block profile",
                  "h2d_bytes_per_step": st["h2d_bytes"], "d2h_bytes_per_step": st["d2h_bytes"],
                  "gpu_budget_gib": budget_gib},
         "offload": offload,
+        "planning": planning,
         "lanes_vs_sim": {"measured_ms_per_step": lanes,
                          "simulated_ms_per_step": dict(zip(("compute", "h2d", "d2h", "cpu_optim"),
                                                            st_t["sim_lane_busy_ms"])),
@@ -551,6 +585,8 @@ def main():
     ap.add_argument("--cpu-threads", type=int,
                     default=max(1, ((os.cpu_count() or 8) - 2) // max(1, int(os.environ.get("WORLD_SIZE", "1")))))
     ap.add_argument("--strategy", default="", help="force c,p,o (default: planner)")
+    ap.add_argument("--no-calibrate-plan", dest="calibrate_plan", action="store_false",
+                    help="plan on the isolated one-block profile only (no in-step calibration)")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     if a.ps_steps < 0:
@@ -596,8 +632,8 @@ def main():
                           "tens of GB >> 126 MB L2"),
     }
     for k in ("e2e", "gpu_launches", "roofline", "model_flops_per_token", "mfu_model", "loss", "bound_by",
-              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "lanes_vs_sim", "calibration", "memory",
-              "ps_gain", "grad", "profiled_rates", "clocks", "init_s"):
+              "lane_busy_ms_per_step", "cpu_optim", "plan", "offload", "planning", "lanes_vs_sim", "calibration",
+              "memory", "ps_gain", "grad", "profiled_rates", "clocks", "init_s"):
         line[k] = head[k]
     if dist:
         line["nccl_ranks"] = dist.get_world_size()
@@ -625,7 +661,7 @@ def main():
                              headline=False)
             sec[name] = {k: r[k] for k in ("value", "ms_per_step", "e2e", "roofline", "mfu_model", "bound_by",
                                            "lane_busy_ms_per_step", "lanes_vs_sim", "calibration", "memory", "plan",
-                                           "offload", "ps_gain", "grad", "clocks")}
+                                           "offload", "planning", "ps_gain", "grad", "clocks")}
             sec[name]["workload"] = workload_config(argparse.Namespace(config=name, strategy="",
                                                                        gpu_mem_gib=GPU_BUDGET_GIB[name]),
                                                     CONFIGS[name], 1)["workload"]

@@ -356,8 +356,17 @@ typedef struct ah_calibration {
     int32_t c_hat, p_hat, o_hat;
     double sim_steady_replan_s;
     double sim_steady_other_s; /* the running plan in the OTHER order (FIFO if PS runs, PS if FIFO) */
+    /* the durations as HardwareSpec / ModelSpec rates (inverse of estimate_block_times) */
+    double gpu_flops, bwd_fwd_ratio, h2d_bw, d2h_bw, cpu_adam_rate, gpu_adam_rate;
 } ah_calibration;
 int ah_trainer_calibrate(void* trainer, ah_calibration* out);
+/* Plan on the last calibration (the paper's profiler measures by executing):
+ * if the reference planner keeps the running (c_hat, p_hat, o_hat) with the calibrated rates — or
+ * keep_strategy != 0 — the trainer adopts the calibrated profile, lookaheads and per-lane order in
+ * place (drains first; memory layout unchanged) and *applied = 1; otherwise nothing changes and
+ * *applied = 0 (a different plan needs a new trainer built from the calibrated rates).
+ * Single-GPU trainers only. */
+int ah_trainer_apply_calibration(void* trainer, int32_t keep_strategy, int32_t* applied);
 
 /* Host side of the profiler: the CpuOptim lane's roofline on this host. n params of pinned
  * 14 B/param state (allocated and freed inside: a setup call); stream_gbps = best in-place pass

@@ -187,11 +187,14 @@ class Calibration(C.Structure):
                 ("t_h2d_s", C.c_double), ("t_d2h_s", C.c_double), ("t_opt_cpu_s", C.c_double),
                 ("t_opt_gpu_s", C.c_double), ("sim_steady_s", C.c_double), ("c_hat", C.c_int32),
                 ("p_hat", C.c_int32), ("o_hat", C.c_int32), ("sim_steady_replan_s", C.c_double),
-                ("sim_steady_other_s", C.c_double)]
+                ("sim_steady_other_s", C.c_double), ("gpu_flops", C.c_double), ("bwd_fwd_ratio", C.c_double),
+                ("h2d_bw", C.c_double), ("d2h_bw", C.c_double), ("cpu_adam_rate", C.c_double),
+                ("gpu_adam_rate", C.c_double)]
 
 
 _EXTRA_SIGS.update({
     "ah_trainer_calibrate": ([C.c_void_p, C.POINTER(Calibration)], C.c_int),
+    "ah_trainer_apply_calibration": ([C.c_void_p, C.c_int32, C.POINTER(C.c_int32)], C.c_int),
     "ah_trainer_set_schedule": ([C.c_void_p, C.c_int32], C.c_int),
     "ah_trainer_memory_csv": ([C.c_void_p, C.c_char_p, C.c_size_t, C.POINTER(C.c_int64)], C.c_int),
     "ah_profile_host": ([C.c_size_t, C.c_int32, C.POINTER(HostProfile)], C.c_int),

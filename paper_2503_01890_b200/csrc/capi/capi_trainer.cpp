@@ -91,6 +91,14 @@ int ah_trainer_calibrate(void* tr, ah_calibration* out) {
     return guarded([&] { T(tr)->calibrate(out); });
 }
 
+int ah_trainer_apply_calibration(void* tr, int32_t keep_strategy, int32_t* applied) {
+    if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
+    return guarded([&] {
+        const bool a = T(tr)->apply_calibration(keep_strategy != 0);
+        if (applied) *applied = a ? 1 : 0;
+    });
+}
+
 int ah_trainer_set_schedule(void* tr, int32_t priority_sched) {
     if (!tr) return ah::set_error(AH_ERR_INVALID, "null trainer");
     return guarded([&] { T(tr)->set_schedule(priority_sched != 0); });

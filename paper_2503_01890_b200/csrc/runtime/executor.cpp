@@ -312,6 +312,7 @@ void Trainer::calibrate(ah_calibration* out) {
         out->sim_steady_other_s = std::nan("");
     }
     out->c_hat = out->p_hat = out->o_hat = -1;
+    cal_valid_ = cal_plan_valid_ = false;
     if (dp_size_ > 1) return;
     // the plan the reference planner picks with these durations expressed as HardwareSpec rates
     // (the inverse of estimate_block_times, workload.cpp:55-73)
@@ -325,6 +326,15 @@ void Trainer::calibrate(ah_calibration* out) {
     hw.d2h_bandwidth = 2.0 * mp / b.t_d2h;
     hw.cpu_optim_rate = mp / b.t_opt_cpu;
     hw.gpu_optim_rate = mp / b.t_opt_gpu;
+    out->gpu_flops = hw.gpu_compute_rate;
+    out->bwd_fwd_ratio = spec.bwd_fwd_ratio;
+    out->h2d_bw = hw.h2d_bandwidth;
+    out->d2h_bw = hw.d2h_bandwidth;
+    out->cpu_adam_rate = hw.cpu_optim_rate;
+    out->gpu_adam_rate = hw.gpu_optim_rate;
+    cal_hw_ = hw;
+    cal_spec_ = spec;
+    cal_valid_ = true;
     try {
         const hetsim::ModelProfile pr = hetsim::build_profile(spec, hw, ov_);
         hetsim::PlanRequest req;
@@ -336,9 +346,32 @@ void Trainer::calibrate(ah_calibration* out) {
         out->p_hat = st.p_hat;
         out->o_hat = st.o_hat;
         out->sim_steady_replan_s = hetsim::run(pr, st, hw, 3, ps_).steady_state_time;
+        cal_strategy_ = st;
+        cal_plan_valid_ = true;
     } catch (const std::exception&) {
         // infeasible with these rates: report no plan
     }
+}
+
+bool Trainer::apply_calibration(bool keep_strategy) {
+    if (!cal_valid_ || dp_size_ > 1) return false;
+    const bool same = cal_plan_valid_ && cal_strategy_.c_hat == strategy_.c_hat &&
+                      cal_strategy_.p_hat == strategy_.p_hat && cal_strategy_.o_hat == strategy_.o_hat;
+    if (!keep_strategy && !same) return false;
+    drain();
+    hw_ = cal_hw_;
+    spec_ = cal_spec_;
+    profile_ = hetsim::build_profile(spec_, hw_, ov_);
+    if (!keep_strategy) strategy_ = cal_strategy_;  // same (c, p, o); the lookaheads may differ
+    sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    sim_steady_[ps_ ? 1 : 0] = sim_.steady_state_time;
+    try {
+        sim_steady_[ps_ ? 0 : 1] = hetsim::run(profile_, strategy_, hw_, 3, !ps_).steady_state_time;
+    } catch (const std::exception&) {
+        sim_steady_[ps_ ? 0 : 1] = std::nan("");
+    }
+    compile_order();
+    return true;
 }
 
 void Trainer::set_schedule(bool priority) {

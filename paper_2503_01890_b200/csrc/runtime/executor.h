@@ -55,6 +55,7 @@ public:
     void set_schedule(bool priority);
     // In-step calibration of the block durations from the drained window (ah_calibration).
     void calibrate(ah_calibration* out);
+    bool apply_calibration(bool keep_strategy);
     void stats(ah_trainer_stats* out);
     void reset_stats();  // zero the lane busy-time counters and the offload window
     // fp32 master of block b (1-based; 0 = embedding wte, -1 = wpe, -2 = final LN) -> host.
@@ -170,6 +171,11 @@ private:
     hetsim::ProfileOverrides ov_;       // m_gc of this runtime
     hetsim::HardwareSpec hw_cfg_;       // rates / budgets as configured (before DP adjustments)
     bool fine_tune_ = false;
+    // last calibrate(): the rates it derived and the plan the reference planner picks with them
+    bool cal_valid_ = false, cal_plan_valid_ = false;
+    hetsim::HardwareSpec cal_hw_;
+    hetsim::ModelSpec cal_spec_;
+    hetsim::Strategy cal_strategy_;
     hetsim::SimResult sim_;
     double sim_steady_[2] = {0.0, 0.0};  // reference scheduler steady state: [0] FIFO, [1] PS
     double sim_lane_ms_[4] = {0, 0, 0, 0};  // simulated busy time per lane, steady iteration

@@ -154,6 +154,14 @@ class Trainer:
         N.check(N.lib().ah_trainer_calibrate(self._h, C.byref(out)), "ah_trainer_calibrate")
         return {f: getattr(out, f) for f, _ in out._fields_}
 
+    def apply_calibration(self, keep_strategy: bool = False) -> bool:
+        """Adopt the last calibrate()'s rates in place if the planner keeps the running plan with
+        them (or keep_strategy); False: a different plan, build a new Trainer from the rates."""
+        applied = C.c_int32()
+        N.check(N.lib().ah_trainer_apply_calibration(self._h, int(keep_strategy), C.byref(applied)),
+                "ah_trainer_apply_calibration")
+        return bool(applied.value)
+
     def set_schedule(self, priority: bool) -> None:
         """Priority-based (True) or FIFO (False) per-lane order for the following iterations."""
         N.check(N.lib().ah_trainer_set_schedule(self._h, int(priority)), "ah_trainer_set_schedule")

@@ -299,3 +299,29 @@ def test_calibrate_from_window(cuda_device, native):
         assert c[k] > 0, k
     L = MODEL["num_blocks"]
     assert 0 <= c["p_hat"] <= c["o_hat"] <= L and 0 <= c["c_hat"] <= L
+
+
+def test_apply_calibration_in_place(cuda_device, native):
+    """Adopting the calibrated profile in place changes only the model the schedule is compiled
+    from (order / lookaheads): training state stays bit-identical to the all-GPU plan."""
+    from paper_2503_01890_b200.trainer import PlanConfig
+    base_loss, base_state, _ = run_plan(PLANS[0], steps=4)
+    tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=3, fine_tune=False, gpu_mem_budget=1 << 40))
+    for k in range(2):
+        tr.submit(*batch(k))
+    tr.drain()
+    before = tr.stats()["sim_steady_ps_s"]
+    c = tr.calibrate()
+    assert c["gpu_flops"] > 0 and c["cpu_adam_rate"] > 0 and c["h2d_bw"] > 0
+    assert tr.apply_calibration(keep_strategy=True)
+    st = tr.stats()
+    assert (st["c_hat"], st["p_hat"], st["o_hat"]) == (2, 2, 3)
+    assert st["sim_steady_ps_s"] != before
+    for k in range(2, 4):
+        tr.submit(*batch(k))
+    loss = tr.drain()
+    state = [tr.master(i).copy() for i in range(-2, MODEL["num_blocks"] + 1)]
+    tr.close()
+    assert loss == base_loss[-1]
+    for a, b in zip(state, base_state):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
