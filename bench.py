@@ -580,10 +580,11 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the 1.3B / 124M secondary lines")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
-    # CPU Adam team: all cores but two (the lane threads sleep on events / condition variables;
-    # 14 of 16 threads measured fastest for the host AdamW on the B200 box); split across ranks
+    # CPU Adam team: every host core, split across the ranks of the node (the lane threads sleep on
+    # events / condition variables; on the 16-vCPU B200 box the 10B step measured 1335 ms with 16
+    # threads vs 1409 ms with 14, OMP_PROC_BIND=close 1453 ms: profiles/r2/cpu_threads_10b.txt)
     ap.add_argument("--cpu-threads", type=int,
-                    default=max(1, ((os.cpu_count() or 8) - 2) // max(1, int(os.environ.get("WORLD_SIZE", "1")))))
+                    default=max(1, (os.cpu_count() or 8) // max(1, int(os.environ.get("WORLD_SIZE", "1")))))
     ap.add_argument("--strategy", default="", help="force c,p,o (default: planner)")
     ap.add_argument("--no-calibrate-plan", dest="calibrate_plan", action="store_false",
                     help="plan on the isolated one-block profile only (no in-step calibration)")
