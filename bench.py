@@ -428,19 +428,27 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
     ps_gain = None
     if a.ps_steps > 0:
         kp = a.ps_steps
-        res = {}
+        res, cals = {}, {}
         for ps in (False, True):
             tr.set_schedule(ps)
             for i in range(2):
                 tr.submit(dev_tok[i % n_batches], dev_tgt[i % n_batches])
             tr.drain()
             res[ps] = timed(kp) / kp
+            cals[ps] = tr.calibrate()  # this window's in-step durations, the running order simulated
         st_ps = tr.stats()
-        cal_ps = tr.calibrate()  # the PS window's in-step durations: the gain the model predicts with them
+        cal_ps = cals[True]
         sim_gain = st_ps["sim_steady_fifo_s"] / st_ps["sim_steady_ps_s"] if st_ps["sim_steady_ps_s"] > 0 else None
+        dur_keys = ("t_fwd_s", "t_bwd_s", "t_h2d_s", "t_d2h_s", "t_opt_cpu_s", "t_opt_gpu_s")
         ps_gain = {"measured": res[False] / res[True], "simulated": sim_gain,
                    "simulated_calibrated": (cal_ps["sim_steady_other_s"] / cal_ps["sim_steady_s"]
                                             if cal_ps["sim_steady_s"] > 0 else None),
+                   # each order simulated with the durations measured while it ran: the lanes share
+                   # host DRAM, so op durations depend on how much the order overlaps them
+                   "simulated_per_window": (cals[False]["sim_steady_s"] / cals[True]["sim_steady_s"]
+                                            if cals[True]["sim_steady_s"] > 0 else None),
+                   "in_step_durations_s": {"fifo": {k: cals[False][k] for k in dur_keys},
+                                           "ps": {k: cals[True][k] for k in dur_keys}},
                    "ms_per_step_ps": res[True], "ms_per_step_fifo": res[False],
                    "sim_steady_ms_ps": st_ps["sim_steady_ps_s"] * 1e3,
                    "sim_steady_ms_fifo": st_ps["sim_steady_fifo_s"] * 1e3, "steps_each": kp,
