@@ -1064,9 +1064,14 @@ void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_devi
     }
     cv_.notify_all();
     for (Iter* old : retired_) {
+        int64_t net = 0;
+        for (auto& kv : old->ops) net += kv.second.alloc_b - kv.second.free_b;
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            retired_bytes_ += net;
+        }
         for (auto& kv : old->ops) {
             RtOp& o = kv.second;
-            retired_bytes_ += o.alloc_b - o.free_b;
             if (o.lane != kCpu && o.host_ms >= 0) {  // account GPU lane time before the events go
                 float ms = 0.f;
                 if (cudaEventSynchronize(o.t1) == cudaSuccess && cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
