@@ -83,10 +83,10 @@ __device__ __forceinline__ void stats_commit(float* stats, float sum, unsigned b
     __threadfence();
 }
 
-// CTA reduction (256 threads) in warp order, then stats_commit.
+// CTA reduction (up to 1024 threads) in warp order, then stats_commit.
 __device__ __forceinline__ void block_stats_commit(float* stats, const Stat& st) {
-    __shared__ float s_sum[8];
-    __shared__ unsigned s_bad[8];
+    __shared__ float s_sum[32];
+    __shared__ unsigned s_bad[32];
     const float ws = warp_sum(st.sumsq);
     const unsigned wb = warp_sum_u(st.nonfinite);
     if ((threadIdx.x & 31) == 0) {
@@ -274,37 +274,42 @@ __global__ void cast_tail_kernel(const float* src, uint16_t* dst, size_t begin, 
         dst[i] = (uint16_t)f32_to_bf16_bits(src[i]);
 }
 
-__global__ void grad_stats_kernel(const uint16_t* __restrict__ g, size_t n, float inv_scale,
-                                  float* __restrict__ stats, bool vec) {
+__global__ void __launch_bounds__(1024, 1) grad_stats_kernel(const uint16_t* __restrict__ g, size_t n, float inv_scale,
+                                                          float* __restrict__ stats, bool vec) {
     pdl_launch_dependents();
     pdl_wait();
-    Stat st;
+    // one 1024-thread CTA per SM (the fixed-order cross-CTA scratch caps the CTA count, so the
+    // CTAs are large), 4 loads in flight per thread (~10 MB device-wide) and 4 independent partial
+    // sums per thread (combined in a fixed order) so the add chains do not serialise
+    constexpr int kU = 4;
+    Stat st[kU];
     const size_t stride = (size_t)gridDim.x * blockDim.x;
     const size_t n_vec = vec ? n / 8 : 0;
-    // kStatsUnroll independent 16-B loads in flight per thread: the grid is capped at
-    // kStatsMaxCtas CTAs (fixed-order reduction scratch), so one load per thread (~1 MB in flight
-    // device-wide) ran at ~2.2 TB/s; the HBM needs several MB in flight
-    constexpr int kStatsUnroll = 8;
-    for (size_t j0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < n_vec; j0 += stride * kStatsUnroll) {
-        uint4 w[kStatsUnroll];
+    for (size_t j0 = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < n_vec; j0 += stride * kU) {
+        uint4 w[kU];
 #pragma unroll
-        for (int u = 0; u < kStatsUnroll; ++u) {
+        for (int u = 0; u < kU; ++u) {
             const size_t j = j0 + (size_t)u * stride;
             w[u] = j < n_vec ? ld_stream_u4(g + j * 8) : make_uint4(0, 0, 0, 0);
         }
 #pragma unroll
-        for (int u = 0; u < kStatsUnroll; ++u) {
+        for (int u = 0; u < kU; ++u) {
             const uint32_t ws[4] = {w[u].x, w[u].y, w[u].z, w[u].w};
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
                 const uint32_t bits = (e & 1) ? (ws[e >> 1] >> 16) : (ws[e >> 1] & 0xffffu);
-                account(st, __fmul_rn(bf16_bits_to_f32(bits), inv_scale));  // zero padding adds +0
+                account(st[u], __fmul_rn(bf16_bits_to_f32(bits), inv_scale));  // zero padding adds +0
             }
         }
     }
     for (size_t i = n_vec * 8 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
-        account(st, __fmul_rn(bf16_bits_to_f32(g[i]), inv_scale));
-    block_stats_commit(stats, st);
+        account(st[0], __fmul_rn(bf16_bits_to_f32(g[i]), inv_scale));
+    Stat t;
+    for (int u = 0; u < kU; ++u) {
+        t.sumsq = __fadd_rn(t.sumsq, st[u].sumsq);
+        t.nonfinite += st[u].nonfinite;
+    }
+    block_stats_commit(stats, t);
 }
 
 bool aligned16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15u) == 0; }
@@ -382,9 +387,8 @@ cudaError_t launch_grad_stats(const uint16_t* g, size_t n, float inv_scale, floa
                               cudaStream_t stream) {
     if (n == 0) return cudaSuccess;
     const bool vec = aligned16(g);
-    int grid = grid_for(vec ? n / 8 + 1 : n, 256, 8);
-    if (grid > kStatsMaxCtas) grid = kStatsMaxCtas;
-    launch_ex(grad_stats_kernel, dim3(grid), dim3(256), 0, stream, 1, g, n, inv_scale, stats, vec);
+    const int grid = grid_for(vec ? n / 32 + 1 : n, 1024, 1);  // <= kNumSMs <= kStatsMaxCtas
+    launch_ex(grad_stats_kernel, dim3(grid), dim3(1024), 0, stream, 1, g, n, inv_scale, stats, vec);
     return launched(1);
 }
 
