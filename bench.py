@@ -166,10 +166,19 @@ class ClockSampler:
                 "source": "nvml" if self._nvml else "nvidia-smi"}
 
 
-def gemm_traffic():
-    """DRAM bytes (read + write) of one representative GEMM launch from the committed
-    `ncu --set full` capture (profiles/r1/gemm_fc_ncu.json: the 8192x8192x2048 MLP GEMM),
-    next to its algorithmic bytes (A + B + C once)."""
+def gemm_traffic(config):
+    """DRAM bytes (read + write) of one representative GEMM launch of the workload from a
+    committed `ncu --set full` capture, next to its algorithmic bytes (A + B + C once): the 10B
+    qkv projection (profiles/r2/gemm_qkv_10b_ncu.json) or the 1.3B MLP GEMM
+    (profiles/r1/gemm_fc_ncu.json)."""
+    if config in ("10b", "20b"):
+        p = os.path.join(ROOT, "profiles", "r2", "gemm_qkv_10b_ncu.json")
+        if not os.path.exists(p):
+            return None
+        d = json.load(open(p))
+        return {"bytes": (d["dram_read_MB"] + d["dram_write_MB"]) * 1e6, "algorithmic_bytes": d["algorithmic_bytes_MB"] * 1e6,
+                "launch": d["shape"], "tensor_pipe_active_pct": d["tensor_pipe_active_pct_elapsed"], "note": d["note"],
+                "source": "profiles/r2/gemm_qkv_10b_ncu.json"}
     p = os.path.join(ROOT, "profiles", "r1", "gemm_fc_ncu.json")
     if not os.path.exists(p):
         return None
@@ -494,7 +503,7 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
                 "sync_step_api": "Trainer.step(): blocks on each step's loss (no cross-iteration overlap)"},
         "gpu_launches": int(launches),
         "roofline": {"bound": "tensor", "achieved": gemm_tflops, "peak": bf16_peak, "unit": "TFLOP/s",
-                     "frac": (gemm_tflops / bf16_peak) if gemm_tflops else None, "traffic": gemm_traffic(),
+                     "frac": (gemm_tflops / bf16_peak) if gemm_tflops else None, "traffic": gemm_traffic(cfg_name),
                      "kernel": "gemm_kernel (tcgen05)", "peak_kind": f"{peak_kind} {'burst' if burst else 'sustained'} bf16",
                      "gemm_share_of_step": g_ms.value / ms_gwin if ms_gwin > 0 else None,
                      "gemm_launches": int(g_n.value),
