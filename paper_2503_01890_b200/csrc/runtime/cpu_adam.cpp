@@ -74,9 +74,12 @@ void cpu_adam(const ah_adam_hparams& hp, float* p, float* m, float* v, const uin
     if (nthreads <= 0) nthreads = omp_get_num_procs();
     // (Non-temporal stores of the bf16 output / of p, m, v were measured slower on the 10B plan:
     // 1512 / 1674 vs 1423 ms per step — the in-place update re-writes lines it just read.)
+    // Chunks are handed out dynamically (4 at a time = 256 KiB runs per stream): the lane threads
+    // share the cores with this team, and under a static split one preempted thread held the
+    // whole op back. Every element is independent, so the assignment does not change a bit.
     constexpr std::size_t kChunk = 16384;  // 64 KiB of fp32 per stream per chunk
     const std::size_t n_chunks = (n + kChunk - 1) / kChunk;
-#pragma omp parallel for schedule(static) num_threads(nthreads) if (n_chunks > 1)
+#pragma omp parallel for schedule(dynamic, 4) num_threads(nthreads) if (n_chunks > 1)
     for (std::size_t c = 0; c < n_chunks; ++c) {
         const std::size_t a = c * kChunk;
         const std::size_t len = (a + kChunk <= n) ? kChunk : n - a;
