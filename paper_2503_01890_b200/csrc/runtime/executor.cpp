@@ -359,17 +359,22 @@ bool Trainer::apply_calibration(bool keep_strategy) {
                       cal_strategy_.p_hat == strategy_.p_hat && cal_strategy_.o_hat == strategy_.o_hat;
     if (!keep_strategy && !same) return false;
     drain();
+    // build everything first (the scheduler may throw), then commit
+    const hetsim::ModelProfile profile = hetsim::build_profile(cal_spec_, cal_hw_, ov_);
+    const hetsim::Strategy strategy = keep_strategy ? strategy_ : cal_strategy_;  // same (c, p, o)
+    hetsim::SimResult sim = hetsim::run(profile, strategy, cal_hw_, 3, ps_);
+    double other = std::nan("");
+    try {
+        other = hetsim::run(profile, strategy, cal_hw_, 3, !ps_).steady_state_time;
+    } catch (const std::exception&) {
+    }
     hw_ = cal_hw_;
     spec_ = cal_spec_;
-    profile_ = hetsim::build_profile(spec_, hw_, ov_);
-    if (!keep_strategy) strategy_ = cal_strategy_;  // same (c, p, o); the lookaheads may differ
-    sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    profile_ = profile;
+    strategy_ = strategy;
+    sim_ = std::move(sim);
     sim_steady_[ps_ ? 1 : 0] = sim_.steady_state_time;
-    try {
-        sim_steady_[ps_ ? 0 : 1] = hetsim::run(profile_, strategy_, hw_, 3, !ps_).steady_state_time;
-    } catch (const std::exception&) {
-        sim_steady_[ps_ ? 0 : 1] = std::nan("");
-    }
+    sim_steady_[ps_ ? 0 : 1] = other;
     compile_order();
     return true;
 }
@@ -377,8 +382,9 @@ bool Trainer::apply_calibration(bool keep_strategy) {
 void Trainer::set_schedule(bool priority) {
     drain();  // every lane idle: the next iteration starts on the new order
     if (priority == ps_) return;
+    hetsim::SimResult sim = hetsim::run(profile_, strategy_, hw_, 3, priority);  // may throw: commit after
     ps_ = priority;
-    sim_ = hetsim::run(profile_, strategy_, hw_, 3, ps_);
+    sim_ = std::move(sim);
     compile_order();
 }
 
