@@ -282,6 +282,10 @@ typedef struct ah_trainer_stats {
     /* the reference scheduler's per-lane busy time of one steady-state iteration (compute, h2d,
      * d2h, cpu; ms) for the plan and order in use — the simulated counterpart of lane_busy_ms */
     double sim_lane_busy_ms[4];
+    /* sub-block streaming of the offload chain GradOffload -> CpuOptim -> ParamPrefetch: chunks
+     * per block vector (1 = whole-block ops; env AH_STREAM_CHUNK_MB sets the chunk size, 16 MB
+     * of bf16 by default, 0 = off) */
+    int32_t stream_chunks;
 } ah_trainer_stats;
 
 int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);

@@ -137,6 +137,7 @@ Trainer::~Trainer() {
             RtOp& o = kv.second;
             for (cudaEvent_t e : {o.done_ev, o.start_ev, o.t0, o.t1})
                 if (e) cudaEventDestroy(e);
+            for (cudaEvent_t e : o.ct) cudaEventDestroy(e);
         }
         delete it;
     }
@@ -170,8 +171,10 @@ Trainer::~Trainer() {
     cudaStreamDestroy(s_side_);
     cudaEventDestroy(ev_c2s_);
     cudaEventDestroy(ev_s2c_);
-    for (BlockState& b : blocks_)
+    for (BlockState& b : blocks_) {
         if (b.mat_ev) cudaEventDestroy(b.mat_ev);
+        for (cudaEvent_t e : b.go_ev) cudaEventDestroy(e);
+    }
     cudaStreamDestroy(s_d2h_);
 }
 
@@ -280,9 +283,8 @@ void Trainer::calibrate(ah_calibration* out) {
                 if (k < 0) continue;
                 double ms = o.host_ms;
                 if (o.lane != kCpu) {
-                    float x = 0.f;
-                    if (cudaEventElapsedTime(&x, o.t0, o.t1) != cudaSuccess) continue;
-                    ms = x;
+                    ms = op_ms(o);
+                    if (ms < 0) continue;
                 }
                 sum[k] += ms / 1e3;
                 cnt[k] += 1;
@@ -436,6 +438,13 @@ void Trainer::allocate_and_init() {
     check(cudaMalloc(&tmpb, mp * 2), "tmp");
     blocks_.assign((size_t)d_.L + 1, BlockState{});
     const int L = d_.L;
+    {   // sub-block streaming of the offload chain: ~16 MB bf16 chunks, at most 16 per block
+        const size_t n = dp_ ? shard_ : mp;
+        double mb = 16.0;
+        if (const char* e = std::getenv("AH_STREAM_CHUNK_MB")) mb = std::atof(e);  // 0 = whole blocks
+        nsub_ = mb > 0 ? (int)std::min<double>(16.0, std::max(1.0, std::floor(2.0 * (double)n / (mb * 1e6)))) : 1;
+        if (n < 2 * 16384) nsub_ = 1;
+    }
     for (int i = 1; i <= L; ++i) {
         BlockState& b = blocks_[(size_t)i];
         b.c = i <= strategy_.c_hat;
@@ -455,6 +464,10 @@ void Trainer::allocate_and_init() {
         const size_t n = dp_ ? shard_ : mp;
         const size_t off = dp_ ? shard_ * (size_t)dp_rank_ : 0;
         const size_t valid = dp_ ? my_len_ : mp;
+        if (b.o && nsub_ > 1) {
+            b.go_ev.assign((size_t)nsub_, nullptr);
+            for (cudaEvent_t& e : b.go_ev) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        }
         if (b.o) {
             // optimizer state in pinned host DRAM: 12 B/param + shared 2 B param/grad buffer
             check(cudaHostAlloc((void**)&b.master, n * 4, cudaHostAllocPortable), "host alloc");
@@ -545,6 +558,14 @@ void Trainer::build_iteration(Iter& it) {
         // weights, which for P-blocks arrive with the backward prefetch.
         if (so.kind == OpKind::Recompute && so.block <= strategy_.p_hat)
             r.deps.push_back({it.k, OpKey{(int)OpKind::ParamPrefetch, so.block, true}});
+        if (nsub_ > 1 && so.kind == OpKind::ParamPrefetch && !so.backward_copy)
+            for (const auto& d : r.deps)
+                if (d.second.kind == (int)OpKind::CpuOptim && d.second.block == so.block) {
+                    r.streamed = true;
+                    r.stream_src = d;
+                    r.ct.assign(2 * (size_t)nsub_, nullptr);
+                    for (cudaEvent_t& e : r.ct) check(cudaEventCreate(&e), "event");
+                }
         check(cudaEventCreateWithFlags(&r.done_ev, cudaEventDisableTiming), "event");
         check(cudaEventCreateWithFlags(&r.start_ev, cudaEventDisableTiming), "event");
         if (r.lane != kCpu) {
@@ -565,7 +586,7 @@ Trainer::RtOp* Trainer::find(long long iter, const OpKey& key) {
     return nullptr;
 }
 
-void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side) {
+void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side, int state_only) {
     if (iter < 1) return;
     cudaEvent_t ev = nullptr;
     int dep_lane = 0;
@@ -575,9 +596,9 @@ void Trainer::wait_dep(int lane, long long iter, const OpKey& key, bool gate, bo
         RtOp* d = find(iter, key);
         if (!d) return;  // retired => long complete
         dep_lane = d->lane;
-        const int need = gate ? 1 : (d->lane == kCpu ? 3 : 2);
+        const int need = state_only > 0 ? state_only : gate ? 1 : (d->lane == kCpu ? 3 : 2);
         cv_.wait(lk, [&] { return d->state >= need || stop_; });
-        if (stop_) return;
+        if (stop_ || state_only > 0) return;
         if (d->lane == kCpu) return;  // host ordering already established
         ev = gate ? d->start_ev : d->done_ev;
         on_side = d->done_on_side;
@@ -611,7 +632,16 @@ void Trainer::lane_main(int lane) {
                 const OpKey& key = it->lane_order[lane][idx];
                 RtOp& op = it->ops.at(key);
                 const bool needs_side = op.kind == OpKind::GpuOptim;
-                for (const auto& dp : op.deps) wait_dep(lane, dp.first, dp.second, false, needs_side);
+                for (const auto& dp : op.deps) {
+                    // sub-block streaming: CpuOptim follows its GradOffload chunk by chunk (the
+                    // copies are issued), a forward prefetch follows the previous iteration's
+                    // CpuOptim chunk by chunk (it started)
+                    int state_only = 0;
+                    if (nsub_ > 1 && op.kind == OpKind::CpuOptim && dp.second.kind == (int)OpKind::GradOffload)
+                        state_only = 2;
+                    if (op.streamed && dp.second.kind == (int)OpKind::CpuOptim) state_only = 1;
+                    wait_dep(lane, dp.first, dp.second, false, needs_side, state_only);
+                }
                 for (const auto& gt : op.gates) wait_dep(lane, gt.first, gt.second, true);
                 if (lane == kCpu) {
                     {
@@ -873,7 +903,16 @@ void Trainer::run_h2d(Iter& it, RtOp& op) {
     check(cudaMallocAsync((void**)&dst, full_len() * 2, s_h2d_), "alloc prefetch");
     op.alloc_b += (int64_t)full_len() * 2;
     uint16_t* mine = dp_ ? dst + shard_ * (size_t)dp_rank_ : dst;
-    if (b.o)
+    if (b.o && op.streamed) {  // chunk c goes up as soon as the host AdamW finished it
+        for (int c = 0; c < nsub_; ++c) {
+            size_t a = 0, len = 0;
+            sub_range(c, n, a, len);
+            wait_progress(op.stream_src.first, op.stream_src.second, c + 1);
+            check(cudaEventRecord(op.ct[2 * (size_t)c], s_h2d_), "record");
+            check(cudaMemcpyAsync(mine + a, b.host_bf16 + a, len * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
+            check(cudaEventRecord(op.ct[2 * (size_t)c + 1], s_h2d_), "record");
+        }
+    } else if (b.o)
         check(cudaMemcpyAsync(mine, b.host_bf16, n * 2, cudaMemcpyHostToDevice, s_h2d_), "prefetch");
     else  // P\O backward prefetch: the fp32 master is on the GPU; materialise without PCIe
         check(launch_cast_f32_bf16(b.master, mine, n, s_h2d_), "prefetch cast");
@@ -887,10 +926,19 @@ void Trainer::run_d2h(Iter& it, RtOp& op) {
     BlockState& b = blocks_[(size_t)op.block];
     const size_t n = dp_ ? shard_ : d_.m_p();
     const uint16_t* src = dp_ ? b.wbuf + shard_ * (size_t)dp_rank_ : b.wbuf;
-    check(cudaMemcpyAsync(b.host_bf16, src, n * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
-    // the block's overflow check rides along: the CPU lane reads it after this op completes
+    // the block's overflow check rides along (first, so it has landed with chunk 0)
     check(cudaMemcpyAsync(gstats_host_ + 2 * op.block, gstats(op.block), 8, cudaMemcpyDeviceToHost, s_d2h_),
           "offload stats");
+    if (nsub_ > 1) {
+        for (int c = 0; c < nsub_; ++c) {
+            size_t a = 0, len = 0;
+            sub_range(c, n, a, len);
+            check(cudaMemcpyAsync(b.host_bf16 + a, src + a, len * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
+            check(cudaEventRecord(b.go_ev[(size_t)c], s_d2h_), "record");
+        }
+    } else {
+        check(cudaMemcpyAsync(b.host_bf16, src, n * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
+    }
     check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
     b.wbuf = nullptr;
     op.free_b += (int64_t)full_len() * 2;
@@ -900,16 +948,64 @@ void Trainer::run_cpu(Iter& it, RtOp& op) {
     BlockState& b = blocks_[(size_t)op.block];
     ah_adam_hparams hp = adam_;
     hp.step = (step_base_ + (int)it.k);
-    const auto t0 = Clock::now();
     const size_t n = dp_ ? shard_ : d_.m_p();
+    double busy = 0.0;  // host AdamW time only (not the waits for gradient chunks)
     uint32_t bad = 0;
-    std::memcpy(&bad, gstats_host_ + 2 * op.block + 1, 4);
-    if (bad == 0) {
-        cpu_adam(hp, b.master, b.m1, b.m2, b.host_bf16, b.host_bf16, n, 1.f / (float)dp_size_, cpu_threads_);
-    } else {  // overflow skip: state untouched; the shared buffer holds grads -> restore bf16(master)
-        cpu_cast_f32_bf16(b.master, b.host_bf16, n, cpu_threads_);
+    for (int c = 0; c < nsub_; ++c) {
+        size_t a = 0, len = 0;
+        sub_range(c, n, a, len);
+        if (nsub_ > 1) check(cudaEventSynchronize(b.go_ev[(size_t)c]), "offload chunk sync");
+        if (c == 0) std::memcpy(&bad, gstats_host_ + 2 * op.block + 1, 4);
+        const auto t0 = Clock::now();
+        if (bad == 0) {
+            cpu_adam(hp, b.master + a, b.m1 + a, b.m2 + a, b.host_bf16 + a, b.host_bf16 + a, len,
+                     1.f / (float)dp_size_, cpu_threads_);
+        } else {  // overflow skip: state untouched; the shared buffer holds grads -> restore bf16(master)
+            cpu_cast_f32_bf16(b.master + a, b.host_bf16 + a, len, cpu_threads_);
+        }
+        busy += std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+        if (nsub_ > 1) {
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                op.progress = c + 1;
+            }
+            cv_.notify_all();
+        }
     }
-    op.host_ms = std::chrono::duration<double, std::milli>(Clock::now() - t0).count();
+    op.host_ms = busy;
+}
+
+// Chunk c of nsub_ over n elements, boundaries on 16384-element (64 KiB fp32) multiples.
+void Trainer::sub_range(int c, size_t n, size_t& a, size_t& len) const {
+    if (nsub_ <= 1) {
+        a = 0;
+        len = n;
+        return;
+    }
+    const size_t q = 16384;
+    const size_t per = round_up((n + (size_t)nsub_ - 1) / (size_t)nsub_, q);
+    a = std::min(n, per * (size_t)c);
+    len = std::min(n, a + per) - a;
+}
+
+void Trainer::wait_progress(long long iter, const OpKey& key, int chunks) {
+    std::unique_lock<std::mutex> lk(mu_);
+    cv_.wait(lk, [&] {
+        if (stop_) return true;
+        const RtOp* d = find(iter, key);
+        return !d || d->state >= 3 || d->progress >= chunks;  // retired => complete
+    });
+}
+
+double Trainer::op_ms(const RtOp& o) const {
+    float x = 0.f;
+    if (o.ct.empty()) return cudaEventElapsedTime(&x, o.t0, o.t1) == cudaSuccess ? x : -1.0;
+    double sum = 0.0;
+    for (size_t c = 0; c + 1 < o.ct.size(); c += 2) {
+        if (cudaEventElapsedTime(&x, o.ct[c], o.ct[c + 1]) != cudaSuccess) return -1.0;
+        sum += x;
+    }
+    return sum;
 }
 
 float* Trainer::gstats(int slot) const { return gstats_dev_ + (size_t)slot * AH_STATS_FLOATS; }
@@ -1079,8 +1175,9 @@ void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_devi
         for (auto& kv : old->ops) {
             RtOp& o = kv.second;
             if (o.lane != kCpu && o.host_ms >= 0) {  // account GPU lane time before the events go
-                float ms = 0.f;
-                if (cudaEventSynchronize(o.t1) == cudaSuccess && cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
+                double ms = -1.0;
+                if (cudaEventSynchronize(o.t1) == cudaSuccess) ms = op_ms(o);
+                if (ms >= 0) {
                     std::lock_guard<std::mutex> lk(mu_);
                     lane_stats_[o.lane].busy_ms += ms;
                     lane_stats_[o.lane].ops += 1;
@@ -1088,6 +1185,7 @@ void Trainer::submit(const int32_t* tokens, const int32_t* targets, bool on_devi
             }
             for (cudaEvent_t e : {o.done_ev, o.start_ev, o.t0, o.t1})
                 if (e) cudaEventDestroy(e);
+            for (cudaEvent_t e : o.ct) cudaEventDestroy(e);
         }
         delete old;
     }
@@ -1111,8 +1209,8 @@ float Trainer::drain() {
             for (auto& kv : it->ops) {
                 RtOp& o = kv.second;
                 if (o.lane == kCpu || o.host_ms < 0) continue;
-                float ms = 0.f;
-                if (cudaEventElapsedTime(&ms, o.t0, o.t1) == cudaSuccess) {
+                const double ms = op_ms(o);
+                if (ms >= 0) {
                     lane_stats_[o.lane].busy_ms += ms;
                     lane_stats_[o.lane].ops += 1;
                 }
@@ -1205,6 +1303,7 @@ void Trainer::stats(ah_trainer_stats* s) {
     s->nonfinite_grads = nonfinite_;
     s->skipped_updates = skipped_;
     for (int l = 0; l < 4; ++l) s->sim_lane_busy_ms[l] = sim_lane_ms_[l];
+    s->stream_chunks = nsub_;
 }
 
 std::string Trainer::trace_json() {
@@ -1544,13 +1643,18 @@ void Trainer::account_window() {
                     const RtOp* d = find(dp.first, dp.second);
                     double ca = 0, cb = 0;
                     if (d && d->lane != kCpu && span(*d, ca, cb) && cb >= sp.cb) {
+                        // a streamed prefetch waits for the host AdamW between chunks: only its
+                        // last chunk's copy is time the link kept the compute lane waiting
+                        float x = 0.f;
+                        if (!d->ct.empty() && cudaEventElapsedTime(&x, origin, d->ct[d->ct.size() - 2]) == cudaSuccess)
+                            ca = x;
                         sp.ca = ca;
                         sp.cb = cb;
                     }
                 }
                 comp.push_back(sp);
             } else if (o.lane == kH2D) {
-                h2d += b - a;
+                h2d += op_ms(o);
                 if (blocks_[(size_t)o.block].o) hb += wbytes;
             } else {
                 d2h += b - a;

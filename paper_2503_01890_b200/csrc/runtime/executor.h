@@ -116,6 +116,14 @@ private:
         double host_ms = 0.0;
         bool done_on_side = false;  // DP backward: done_ev follows the gradient reduce-scatter on s_side_
         int64_t alloc_b = 0, free_b = 0;  // stream-ordered pool bytes taken at its start / returned at its end
+        // Sub-block streaming (nsub_ > 1). CpuOptim: chunks of the block updated so far (the
+        // next iteration's forward ParamPrefetch copies chunk c up as soon as progress > c).
+        // Streamed ParamPrefetch: the CpuOptim it follows, and per-chunk copy timing events
+        // (start, end) so its busy time excludes the waits for the CPU between chunks.
+        int progress = 0;
+        bool streamed = false;
+        std::pair<long long, OpKey> stream_src{0, OpKey{0, 0, false}};
+        std::vector<cudaEvent_t> ct;
     };
     struct Iter {
         long long k = 0;
@@ -137,6 +145,7 @@ private:
         bool needs_gather = false;      // DP: wbuf holds only this rank's shard so far
         cudaEvent_t mat_ev = nullptr;   // side-stream materialisation (cast [+ all-gather]) done
         bool mat_pending = false;       // wbuf was materialised ahead on s_side_; compute must wait mat_ev
+        std::vector<cudaEvent_t> go_ev; // O blocks, nsub_ > 1: GradOffload chunk c landed in host_bf16
     };
 
     void plan(const ah_trainer_config& cfg);
@@ -144,7 +153,9 @@ private:
     void reserve_pool();
     void build_iteration(Iter& it);
     void lane_main(int lane);
-    void wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side = false);
+    // state_only > 0: wait until the dependency reached that state (1 started, 2 issued) and
+    // leave the data dependency to the caller (sub-block streaming)
+    void wait_dep(int lane, long long iter, const OpKey& key, bool gate, bool needs_side = false, int state_only = 0);
     // Side stream: materialisation of the next compute op's weights (overlapping the current
     // op) and every NCCL collective, issued by the compute lane thread in op order.
     void prefetch_weights(const Iter& it, size_t idx, RtOp& cur);
@@ -155,6 +166,15 @@ private:
     void run_h2d(Iter& it, RtOp& op);
     void run_d2h(Iter& it, RtOp& op);
     void run_cpu(Iter& it, RtOp& op);
+    // Sub-block streaming of the offload chain GradOffload -> CpuOptim -> next forward
+    // ParamPrefetch of an O block: the block vector is cut into nsub_ contiguous chunks; the
+    // host AdamW starts on chunk 0 as soon as its D2H copy landed, and the prefetch sends chunk
+    // c up as soon as the host AdamW finished it. Per-lane op order and every dependency of the
+    // reference DAG are kept; only the tail of one op overlaps the head of the next.
+    int nsub_ = 1;
+    void sub_range(int c, size_t n, size_t& a, size_t& len) const;
+    void wait_progress(long long iter, const OpKey& key, int chunks);
+    double op_ms(const RtOp& o) const;  // lane busy time of a GPU-lane op (chunk sum when streamed)
     void embed_forward(Iter& it);
     void head_forward_backward(Iter& it);
     void embed_backward_and_update(Iter& it);

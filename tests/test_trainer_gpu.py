@@ -93,6 +93,25 @@ def test_plans_give_bit_identical_training_state(cuda_device, native):
                 assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), (plan, ps)
 
 
+def test_streamed_offload_chain_is_bit_identical(cuda_device, native, monkeypatch):
+    """Sub-block streaming (GradOffload -> host AdamW -> next forward ParamPrefetch chunk by
+    chunk) changes when bytes move, not what is computed: offloading plans under PS and FIFO,
+    and the DP collective path, give the all-GPU plan's training state bit for bit."""
+    base_loss, base_state, _ = run_plan(PLANS[0])
+    monkeypatch.setenv("AH_STREAM_CHUNK_MB", "0.1")  # 1.58 MB bf16 block -> 15 chunks
+    for plan, ps, fc in ((PLANS[2], True, False), (PLANS[4], True, False), (PLANS[4], False, False),
+                         (PLANS[3], True, True)):
+        loss, state, st = run_plan(plan, ps=ps, fc=fc)
+        assert st["stream_chunks"] > 4, st["stream_chunks"]
+        assert loss == base_loss, (plan, ps, fc)
+        for a, b in zip(state, base_state):
+            n = min(a.size, b.size)
+            assert np.array_equal(a[:n].view(np.uint32), b[:n].view(np.uint32)), (plan, ps, fc)
+    monkeypatch.setenv("AH_STREAM_CHUNK_MB", "0")
+    _, _, st = run_plan(PLANS[2], steps=1)
+    assert st["stream_chunks"] == 1
+
+
 def test_realised_lane_order_matches_scheduler(cuda_device, native):
     from paper_2503_01890_b200.trainer import PlanConfig
     tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=4, priority_sched=True, fine_tune=False,
@@ -175,7 +194,8 @@ def test_long_run_is_deterministic_and_finite(cuda_device, native):
     assert runs[0][-1] < runs[0][0] - 0.5  # it learns
 
 
-def test_overflow_check_skips_every_update(cuda_device, native, tmp_path):
+@pytest.mark.parametrize("chunk_mb", ["16", "0.1"])  # whole-block / streamed offload chain
+def test_overflow_check_skips_every_update(cuda_device, native, tmp_path, monkeypatch, chunk_mb):
     """A NaN in block 2's weights makes every gradient group non-finite: the per-block overflow
     check (grad_stats pre-pass -> skip flag) must leave all optimizer state untouched — GPU
     blocks, host-optimizer blocks (whose shared buffer is restored to bf16(master)) and the
@@ -184,6 +204,7 @@ def test_overflow_check_skips_every_update(cuda_device, native, tmp_path):
     from paper_2503_01890_b200.trainer import PlanConfig
     L, h = MODEL["num_blocks"], MODEL["hidden"]
     mp = 12 * h * h + 13 * h
+    monkeypatch.setenv("AH_STREAM_CHUNK_MB", chunk_mb)
     plan = PlanConfig(fine_tune=False, gpu_mem_budget=1 << 40, c_hat=1, p_hat=1, o_hat=2)  # blocks 3, 4 on the CPU
     tr = make(plan=plan)
     tr.step(*batch(0))
