@@ -5,8 +5,9 @@ Headline workload (BASELINE.json configs[2]; the largest single-GPU config): GPT
 (L=25, h=6144, 48 heads, s=1024, b=8 per GPU, V=50257) under an 80 GiB GPU budget, the paper's
 large-model regime: the planner, fed with rates measured on this box, keeps
 optimizer states of the last blocks in pinned host DRAM (CpuOptim), prefetches bf16 params and
-recomputes activations. Secondary lines (N=1): configs[1] 1.3B at 32 GiB and configs[0]'s
-124M shape under full optimizer offload (0, 0, 12). Synthetic tokens, random-init weights.
+recomputes activations. Secondary lines (N=1): the same 10B model planned against 170 GiB (the
+whole B200 HBM: the planner keeps most optimizer state on the GPU), configs[1] 1.3B at 32 GiB and
+configs[0]'s 124M shape under full optimizer offload (0, 0, 12). Synthetic tokens, random-init weights.
 
   value     tokens/s, whole job (sum over ranks), inputs resident in HBM, device-timed with
             CUDA events on the executor's compute stream bracketing K drained iterations.
@@ -43,6 +44,8 @@ os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 CONFIGS = {
     # configs[2]: the paper's large-model regime (Table 1 row L=25, h=6144)
     "10b": dict(num_blocks=25, hidden=6144, heads=48, seq_len=1024, batch=8, vocab=50257),
+    # the same model planned against (almost) the whole B200 HBM instead of the paper-regime budget
+    "10b_hbm": dict(num_blocks=25, hidden=6144, heads=48, seq_len=1024, batch=8, vocab=50257),
     "1.3b": dict(num_blocks=24, hidden=2048, heads=16, seq_len=1024, batch=8, vocab=50257),
     "124m": dict(num_blocks=12, hidden=768, heads=6, seq_len=512, batch=4, vocab=50257),
     "tiny": dict(num_blocks=4, hidden=256, heads=2, seq_len=256, batch=2, vocab=1000),
@@ -50,10 +53,10 @@ CONFIGS = {
     "20b": dict(num_blocks=26, hidden=8192, heads=64, seq_len=1024, batch=1, vocab=50257),
 }
 # default GPU-memory budget per workload (GiB): memory-constrained so the planner offloads
-GPU_BUDGET_GIB = {"10b": 80, "1.3b": 32, "124m": 8, "tiny": 4, "20b": 170}
+GPU_BUDGET_GIB = {"10b": 80, "10b_hbm": 170, "1.3b": 32, "124m": 8, "tiny": 4, "20b": 170}
 # forced strategies (configs[0]: "full optimizer offload" = (0, 0, L))
 FORCED = {"124m": (0, 0, 12)}
-WORKLOAD = {"10b": "configs[2]", "1.3b": "configs[1]", "124m": "configs[0] shape", "20b": "configs[3] model",
+WORKLOAD = {"10b": "configs[2]", "10b_hbm": "configs[2] model, full-HBM budget", "1.3b": "configs[1]", "124m": "configs[0] shape", "20b": "configs[3] model",
             "tiny": "test"}
 METRIC = "train tokens/s (GPT, planned offload)"
 
@@ -300,7 +303,7 @@ def reference_arm(a, m):
 
 def workload_config(a, m, world):
     forced = a.strategy or (",".join(map(str, FORCED[a.config])) if a.config in FORCED else "")
-    return {"workload": f"{WORKLOAD.get(a.config, a.config)}: GPT-{a.config} (L={m['num_blocks']}, h={m['hidden']}, "
+    return {"workload": f"{WORKLOAD.get(a.config, a.config)}: GPT-{a.config.split('_')[0]} (L={m['num_blocks']}, h={m['hidden']}, "
                         f"heads={m['heads']}, s={m['seq_len']}, b={m['batch']}/GPU, V={m['vocab']}) "
                         + (f"forced strategy ({forced})" if forced else "planned offload")
                         + f" at {a.gpu_mem_gib} GiB GPU budget",
@@ -595,7 +598,7 @@ def main():
     ap.add_argument("--ps-steps", type=int, default=-1, help="PS-vs-FIFO steps each (default min(steps, 8))")
     ap.add_argument("--gemm-window", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-secondary", action="store_true", help="skip the 1.3B / 124M secondary lines")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the 10B full-HBM / 1.3B / 124M secondary lines")
     ap.add_argument("--launch-check", action="store_true", help=argparse.SUPPRESS)
     # CPU Adam team: every host core, split across the ranks of the node (the lane threads sleep on
     # events / condition variables; on the 16-vCPU B200 box the 10B step measured 1335 ms with 16
@@ -671,10 +674,11 @@ def main():
         except Exception as e:  # noqa: BLE001
             line["host_roofline"] = {"error": str(e)}
 
-    # secondary workloads (N = 1): configs[1] and configs[0]'s shape under full optimizer offload
+    # secondary workloads (N = 1): the 10B model planned against the whole HBM, configs[1], and
+    # configs[0]'s shape under full optimizer offload
     if world == 1 and not a.no_secondary and a.config == "10b":
         sec = {}
-        for name in ("1.3b", "124m"):
+        for name in ("10b_hbm", "1.3b", "124m"):
             r = run_workload(a, name, GPU_BUDGET_GIB[name], a.steps, a.warmup, rank, world, local, None,
                              headline=False)
             sec[name] = {k: r[k] for k in ("value", "ms_per_step", "e2e", "roofline", "mfu_model", "bound_by",
