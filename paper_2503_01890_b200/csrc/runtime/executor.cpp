@@ -266,8 +266,12 @@ void Trainer::calibrate(ah_calibration* out) {
     double sum[7] = {0}, cnt[7] = {0};  // F, B, R, H2D, D2H, CPU, GPU-opt
     {
         std::lock_guard<std::mutex> lk(mu_);
+        // a trainer's first iteration runs an empty pipeline and pays one-time costs (lazy module
+        // loading of every kernel, first tensor maps): it is left out when later ones are in the window
+        const bool skip_first = iters_.size() > 1;
         for (Iter* it : iters_)
             for (auto& kv : it->ops) {
+                if (skip_first && it->k == 1) continue;
                 const RtOp& o = kv.second;
                 int k = -1;
                 switch (o.kind) {
