@@ -1,7 +1,7 @@
 /* autohete.h — C-ABI data plane of the B200-native AutoHete hot path.
  *
  * The reference (arXiv 2503.01890, /root/reference/proj) plans and SIMULATES one training
- * iteration: its hetsim::core API (include/hetsim/*.hpp here, drop-in) decides
+ * iteration: its hetsim::core API (include/hetsim/ headers here, drop-in) decides
  * (c_hat, p_hat, o_hat, prefetch_lookahead) and the per-lane op order, and models every op
  * only as a duration. This header is the layer beneath it that EXECUTES those ops on B200.
  * Each entry point names the reference op / interface it realises (file:line in

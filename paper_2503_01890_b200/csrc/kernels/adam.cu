@@ -105,8 +105,6 @@ __device__ __forceinline__ void block_stats_commit(float* stats, const Stat& st)
     }
 }
 
-constexpr int kThreads = 256;
-
 // The update kernel: a persistent CTA per SM streams tiles of kTile params
 // (p, m, v fp32 + g bf16 = 14 B/param) HBM -> shared memory with 1-D bulk copies
 // (cp.async.bulk ... mbarrier::complete_tx) issued by one producer thread into a kStages-deep

@@ -55,14 +55,6 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
     return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
-// Row r's 64 keys of half `half` (32 packed bf16 pairs) into a K-major SWIZZLE_128B tile.
-__device__ __forceinline__ void sts_row_half(uint8_t* tile, int half, int r, const uint32_t (&w)[32]) {
-    uint8_t* rowp = tile + half * (kTile / 2) + r * 128;
-#pragma unroll
-    for (int k8 = 0; k8 < 8; ++k8)
-        *reinterpret_cast<uint4*>(rowp + ((k8 ^ (r & 7)) << 4)) = make_uint4(w[4 * k8], w[4 * k8 + 1], w[4 * k8 + 2], w[4 * k8 + 3]);
-}
-
 __device__ __forceinline__ void load_tile(uint32_t dst, const CUtensorMap* m, uint32_t bar, int row, int head, int b) {
     tma_load_4d(dst, m, bar, 0, row, head, b);
     tma_load_4d(dst + kTile / 2, m, bar, 64, row, head, b);

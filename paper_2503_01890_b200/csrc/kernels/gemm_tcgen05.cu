@@ -1206,7 +1206,7 @@ cudaError_t run(const GemmArgs& g, cudaStream_t stream, int max_ctas) {
         cudaEventRecord(tb, stream);
         std::lock_guard<std::mutex> lk(timing().mu);
         char shape[160];
-        std::snprintf(shape, sizeof shape, "M=%d N=%d K=%d z=%d a_mn=%d b_mn=%d causal=%d epi=%d f32=%d BN=%d CS=%d sk=%d grid=%d",
+        std::snprintf(shape, sizeof shape, "M=%lld N=%lld K=%lld z=%d a_mn=%d b_mn=%d causal=%d epi=%d f32=%d BN=%d CS=%d sk=%d grid=%d",
                       g.M, g.N, g.K, g.batch1 * (g.batch2 > 0 ? g.batch2 : 1), g.a_mn_major, g.b_mn_major, g.causal,
                       g.epilogue, g.c_f32, BN, CS, (int)P.sk, grid);
         timing().recs.push_back({ta, tb, executed_flops(g), shape});
