@@ -356,14 +356,23 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
                 }
                 const float mb = m_used * sl2;
                 float w[kC / 2];  // packed bf16 pairs, bit-cast to float for tcgen05.st
-                float ad[4] = {0.f, 0.f, 0.f, 0.f};
+                unsigned long long ad2[2] = {0ull, 0ull};  // (even, odd) column partial sums
+                const unsigned long long s2 = f2pack(sl2, sl2), nb2 = f2pack(-mb, -mb);
 #pragma unroll
                 for (int i = 0; i < kC / 2; ++i) {
-                    const float p0 = ex2_approx(fmaf(v[2 * i], sl2, -mb)), p1 = ex2_approx(fmaf(v[2 * i + 1], sl2, -mb));
-                    ad[i & 3] += p0 + p1;
+                    float x0, x1;
+                    f2unpack(ffma2(f2pack(v[2 * i], v[2 * i + 1]), s2, nb2), x0, x1);
+                    const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
+                    const unsigned long long p2 = f2pack(p0, p1);
+                    ad2[i & 1] = fadd2(ad2[i & 1], p2);
                     w[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
                 }
-                l += (ad[0] + ad[1]) + (ad[2] + ad[3]);
+                {
+                    float a0, a1, a2, a3;
+                    f2unpack(ad2[0], a0, a1);
+                    f2unpack(ad2[1], a2, a3);
+                    l += (a0 + a1) + (a2 + a3);
+                }
                 if (__any_sync(0xffffffffu, rescale)) {  // O += P V of tile g-1 must have landed
                     mbar_wait(smem_u32(pv_done), (g - 1) & 1);
                     fence_after();
@@ -662,11 +671,15 @@ flash_bwd_t_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constan
                     fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(smem_u32(s_free));
+                    const unsigned long long s2 = f2pack(sl2, sl2);
 #pragma unroll
                     for (int k = 0; k < 16; ++k) {
                         const float4 l4 = reinterpret_cast<const float4*>(lse)[k];
-                        w[2 * k] = pack_bf16x2_rn(ex2_approx(fmaf(v[4 * k], sl2, -l4.x)), ex2_approx(fmaf(v[4 * k + 1], sl2, -l4.y)));
-                        w[2 * k + 1] = pack_bf16x2_rn(ex2_approx(fmaf(v[4 * k + 2], sl2, -l4.z)), ex2_approx(fmaf(v[4 * k + 3], sl2, -l4.w)));
+                        float x0, x1, x2, x3;
+                        f2unpack(ffma2(f2pack(v[4 * k], v[4 * k + 1]), s2, f2pack(-l4.x, -l4.y)), x0, x1);
+                        f2unpack(ffma2(f2pack(v[4 * k + 2], v[4 * k + 3]), s2, f2pack(-l4.z, -l4.w)), x2, x3);
+                        w[2 * k] = pack_bf16x2_rn(ex2_approx(x0), ex2_approx(x1));
+                        w[2 * k + 1] = pack_bf16x2_rn(ex2_approx(x2), ex2_approx(x3));
                     }
                 }
                 if (qi == kt) {  // diagonal tile: P = 0 where the query precedes the key

@@ -43,6 +43,7 @@
 #include "common.cuh"
 #include "gemm.h"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace ah {
 namespace gemm {
@@ -199,6 +200,37 @@ __device__ __forceinline__ float gelu_grad(float x) {
 __device__ __forceinline__ float gelu_tanh(float x) {
     const float k0 = 0.7978845608028654f, k1 = 0.044715f;
     return 0.5f * x * (1.f + tanh_fast(k0 * (x + k1 * x * x * x)));
+}
+
+// The same two GELU functions on a pair of values with paired fp32 arithmetic (FFMA2 / FMUL2:
+// the lean epilogue is issue-bound and its issue slots are shared with the MMA / TMA issuers).
+__device__ __forceinline__ void gelu_tanh2(float& x0, float& x1) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const unsigned long long x = tc::f2pack(x0, x1);
+    const unsigned long long x2 = tc::fmul2(x, x);
+    const unsigned long long t = tc::ffma2(x2, tc::f2pack(k0 * k1, k0 * k1), tc::f2pack(k0, k0));  // k0 (1 + k1 x^2)
+    float u0, u1;
+    tc::f2unpack(tc::fmul2(x, t), u0, u1);
+    const unsigned long long th = tc::f2pack(tanh_fast(u0), tanh_fast(u1));
+    const unsigned long long hx = tc::fmul2(x, tc::f2pack(0.5f, 0.5f));
+    tc::f2unpack(tc::ffma2(hx, th, hx), x0, x1);  // 0.5 x (1 + th)
+}
+
+// v0, v1 *= gelu'(x0), gelu'(x1)
+__device__ __forceinline__ void mul_gelu_grad2(float& v0, float& v1, float x0, float x1) {
+    const float k0 = 0.7978845608028654f, k1 = 0.044715f;
+    const unsigned long long x = tc::f2pack(x0, x1);
+    const unsigned long long x2 = tc::fmul2(x, x);
+    const unsigned long long t = tc::ffma2(x2, tc::f2pack(k0 * k1, k0 * k1), tc::f2pack(k0, k0));
+    float u0, u1;
+    tc::f2unpack(tc::fmul2(x, t), u0, u1);
+    const float t0 = tanh_fast(u0), t1 = tanh_fast(u1);
+    const unsigned long long th = tc::f2pack(t0, t1);
+    const unsigned long long a = tc::ffma2(th, tc::f2pack(0.5f, 0.5f), tc::f2pack(0.5f, 0.5f));     // 0.5 (1 + th)
+    const unsigned long long s = tc::ffma2(tc::f2pack(-t0, -t1), th, tc::f2pack(1.f, 1.f));       // 1 - th^2
+    const unsigned long long d = tc::ffma2(x2, tc::f2pack(3.f * k0 * k1, 3.f * k0 * k1), tc::f2pack(k0, k0));  // k0 (1 + 3 k1 x^2)
+    const unsigned long long b = tc::fmul2(tc::fmul2(x, tc::f2pack(0.5f, 0.5f)), s);              // 0.5 x (1 - th^2)
+    tc::f2unpack(tc::fmul2(tc::f2pack(v0, v1), tc::ffma2(b, d, a)), v0, v1);
 }
 
 struct Tile {
@@ -619,8 +651,9 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                                 const uint4 q4 = a4[w];
                                 const uint32_t u[4] = {q4.x, q4.y, q4.z, q4.w};
 #pragma unroll
-                                for (int e = 0; e < 8; ++e)
-                                    v[8 * w + e] *= gelu_grad(__uint_as_float((e & 1) ? (u[e >> 1] & 0xffff0000u) : (u[e >> 1] << 16)));
+                                for (int e = 0; e < 4; ++e)
+                                    mul_gelu_grad2(v[8 * w + 2 * e], v[8 * w + 2 * e + 1], __uint_as_float(u[e] << 16),
+                                                   __uint_as_float(u[e] & 0xffff0000u));
                             }
                         } else {
 #pragma unroll
@@ -631,7 +664,7 @@ gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
                     if ((P.epi & kEpiGelu) && !(P.epi & kEpiGeluBwd)) {
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] = gelu_tanh(v[j]);
+                        for (int j = 0; j < 32; j += 2) gelu_tanh2(v[j], v[j + 1]);
                     }
                     if (P.epi & kEpiResidual) {
                         const uint4* r4 = reinterpret_cast<const uint4*>(P.res + zr + (long long)m * P.ld_res + n0);
