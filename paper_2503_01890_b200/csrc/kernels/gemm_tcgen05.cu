@@ -184,11 +184,14 @@ __device__ __forceinline__ float tanh_fast(float x) {
     return y;
 }
 
-// v[base .. base+8) += 8 bf16 values packed in w
+// v[base .. base+8) += 8 bf16 values packed in w (paired adds: two columns per FADD2)
 __device__ __forceinline__ void add8(float (&v)[32], int base, uint4 w) {
     const uint32_t u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-    for (int e = 0; e < 8; ++e) v[base + e] += bf16_bits_to_f32((e & 1) ? (u[e >> 1] >> 16) : (u[e >> 1] & 0xffffu));
+    for (int e = 0; e < 4; ++e)
+        tc::f2unpack(tc::fadd2(tc::f2pack(v[base + 2 * e], v[base + 2 * e + 1]),
+                               tc::f2pack(__uint_as_float(u[e] << 16), __uint_as_float(u[e] & 0xffff0000u))),
+                     v[base + 2 * e], v[base + 2 * e + 1]);
 }
 
 __device__ __forceinline__ float gelu_grad(float x) {

@@ -323,28 +323,42 @@ __global__ void __launch_bounds__(768) ln_bwd_rows_kernel(const uint16_t* __rest
         R.mu = mr.x;
         R.rs = mr.y;
         const float nb = -R.mu * R.rs;
-        float s1 = 0.f, s2 = 0.f;
+        // paired fp32 (FFMA2 / FADD2 / FMUL2): the row loop is issue-bound
+        const unsigned long long rs2 = tc::f2pack(R.rs, R.rs), nb2 = tc::f2pack(nb, nb);
+        unsigned long long s1 = 0ull, s2 = 0ull;  // (even, odd) column partial sums
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            R.xf[i] = fmaf(R.xf[i], R.rs, nb);  // xhat
-            const float dg = R.df[i] * gg[i];
-            s1 += dg;
-            s2 = fmaf(dg, R.xf[i], s2);
-            adg[i] = fmaf(R.df[i], R.xf[i], adg[i]);
-            adb[i] += R.df[i];
+        for (int i = 0; i < 8; i += 2) {
+            const unsigned long long xh = tc::ffma2(tc::f2pack(R.xf[i], R.xf[i + 1]), rs2, nb2);  // xhat
+            const unsigned long long d = tc::f2pack(R.df[i], R.df[i + 1]);
+            const unsigned long long dg = tc::fmul2(d, tc::f2pack(gg[i], gg[i + 1]));
+            s1 = tc::fadd2(s1, dg);
+            s2 = tc::ffma2(dg, xh, s2);
+            unsigned long long ag = tc::ffma2(d, xh, tc::f2pack(adg[i], adg[i + 1]));
+            unsigned long long ab = tc::fadd2(tc::f2pack(adb[i], adb[i + 1]), d);
+            tc::f2unpack(xh, R.xf[i], R.xf[i + 1]);
+            tc::f2unpack(ag, adg[i], adg[i + 1]);
+            tc::f2unpack(ab, adb[i], adb[i + 1]);
         }
+        float a0, a1, b0, b1;
+        tc::f2unpack(s1, a0, a1);
+        tc::f2unpack(s2, b0, b1);
         if (lo) {
-            sums.x = s1;
-            sums.y = s2;
+            sums.x = a0 + a1;
+            sums.y = b0 + b1;
         } else {
-            sums.z = s1;
-            sums.w = s2;
+            sums.z = a0 + a1;
+            sums.w = b0 + b1;
         }
     };
     auto emit = [&](const BwdRow<kRes>& R, int j, float m1, float m2) {
         float o[8];
+        const unsigned long long nm2 = tc::f2pack(-m2, -m2), nm1 = tc::f2pack(-m1, -m1), rs2 = tc::f2pack(R.rs, R.rs);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = R.rs * (fmaf(-R.xf[i], m2, R.df[i] * gg[i]) - m1);
+        for (int i = 0; i < 8; i += 2) {
+            const unsigned long long dg = tc::fmul2(tc::f2pack(R.df[i], R.df[i + 1]), tc::f2pack(gg[i], gg[i + 1]));
+            const unsigned long long t = tc::fadd2(tc::ffma2(tc::f2pack(R.xf[i], R.xf[i + 1]), nm2, dg), nm1);
+            tc::f2unpack(tc::fmul2(rs2, t), o[i], o[i + 1]);
+        }
         if (kRes) {
             float rf[8];
             unpack8(R.rw, rf);
