@@ -257,7 +257,7 @@ typedef struct ah_trainer_stats {
     double sim_steady_s;          /* hetsim::run steady-state iteration time */
     double lane_busy_ms[4];       /* compute, h2d, d2h, cpu: summed op time since reset */
     int32_t lane_ops[4];
-    int64_t h2d_bytes, d2h_bytes; /* parameter prefetch / grad offload bytes per iteration */
+    int64_t h2d_bytes, d2h_bytes; /* host-link bytes per iteration: parameter prefetch / grad offload */
     int32_t kernels_per_iter;     /* our kernel launches per iteration */
     /* Offload overlap over the last drained window (CUDA-event timestamps): compute-lane time
      * spent waiting for a ParamPrefetch / GradOffload / CpuOptim dependency, and the busy time

@@ -1287,7 +1287,10 @@ void Trainer::stats(ah_trainer_stats* s) {
         s->lane_ops[l] = lane_stats_[l].ops;
     }
     const int64_t per_block = dp_ ? (int64_t)shard_ : profile_.block.m_p;  // host-link elements
-    s->h2d_bytes = 2 * per_block * (strategy_.o_hat + std::max(0, strategy_.p_hat));
+    // host-link bytes: every O block's forward prefetch, plus the backward re-fetch of the P blocks
+    // that are also O (a P block outside O re-materialises from its GPU master, no PCIe)
+    const int p_and_o = std::max(0, strategy_.p_hat + strategy_.o_hat - d_.L);
+    s->h2d_bytes = 2 * per_block * (strategy_.o_hat + p_and_o);
     s->d2h_bytes = 2 * per_block * strategy_.o_hat;
     s->window_iters = win_iters_;
     s->compute_busy_ms = win_compute_ms_;
