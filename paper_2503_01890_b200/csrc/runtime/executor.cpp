@@ -1297,7 +1297,7 @@ void Trainer::stats(ah_trainer_stats* s) {
     s->h2d_busy_ms = win_h2d_ms_;
     s->d2h_busy_ms = win_d2h_ms_;
     s->offload_blocked_ms = win_blocked_ms_;
-    s->h2d_gbps = win_h2d_ms_ > 0 ? win_h2d_bytes_ / (win_h2d_ms_ * 1e6) : 0.0;
+    s->h2d_gbps = win_h2d_link_ms_ > 0 ? win_h2d_bytes_ / (win_h2d_link_ms_ * 1e6) : 0.0;
     s->d2h_gbps = win_d2h_ms_ > 0 ? win_d2h_bytes_ / (win_d2h_ms_ * 1e6) : 0.0;
     s->copy_blocked_ms = win_copy_blocked_ms_;
     s->upstream_blocked_ms = win_upstream_blocked_ms_;
@@ -1594,7 +1594,7 @@ void Trainer::reset_stats() {
     std::lock_guard<std::mutex> lk(mu_);
     for (LaneStats& l : lane_stats_) l = LaneStats{};
     win_iters_ = win_compute_ms_ = win_h2d_ms_ = win_d2h_ms_ = win_blocked_ms_ = 0;
-    win_h2d_bytes_ = win_d2h_bytes_ = 0;
+    win_h2d_bytes_ = win_d2h_bytes_ = win_h2d_link_ms_ = 0;
     win_copy_blocked_ms_ = win_upstream_blocked_ms_ = win_cpu_ms_ = win_span_ms_ = 0;
 }
 
@@ -1629,7 +1629,7 @@ void Trainer::account_window() {
         double ca, cb;  // the awaited copy's span (latest-finishing offload dependency)
     };
     std::vector<Span> comp;
-    double h2d = 0, d2h = 0, hb = 0, db = 0, cpu = 0;
+    double h2d = 0, d2h = 0, hb = 0, db = 0, cpu = 0, h2d_link = 0;
     const double wbytes = 2.0 * (double)(dp_ ? shard_ : d_.m_p());
     for (Iter* it : iters_)
         for (auto& kv : it->ops) {
@@ -1661,8 +1661,12 @@ void Trainer::account_window() {
                 }
                 comp.push_back(sp);
             } else if (o.lane == kH2D) {
-                h2d += op_ms(o);
-                if (blocks_[(size_t)o.block].o) hb += wbytes;
+                const double ms = op_ms(o);
+                h2d += ms;
+                if (blocks_[(size_t)o.block].o) {  // a PCIe copy (a P block outside O is a GPU cast)
+                    hb += wbytes;
+                    h2d_link += ms;
+                }
             } else {
                 d2h += b - a;
                 db += wbytes;
@@ -1689,6 +1693,7 @@ void Trainer::account_window() {
     win_cpu_ms_ = cpu;
     win_span_ms_ = comp.empty() ? 0.0 : comp.back().b - comp.front().a;
     win_h2d_bytes_ = hb;
+    win_h2d_link_ms_ = h2d_link;
     win_d2h_bytes_ = db;
 }
 

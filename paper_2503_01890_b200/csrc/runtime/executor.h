@@ -248,7 +248,7 @@ private:
     float last_loss_ = 0.f;
     // offload-overlap accounting of the last drain (see ah_trainer_stats)
     double win_iters_ = 0, win_compute_ms_ = 0, win_h2d_ms_ = 0, win_d2h_ms_ = 0, win_blocked_ms_ = 0;
-    double win_h2d_bytes_ = 0, win_d2h_bytes_ = 0;
+    double win_h2d_bytes_ = 0, win_d2h_bytes_ = 0, win_h2d_link_ms_ = 0;
     double win_copy_blocked_ms_ = 0, win_upstream_blocked_ms_ = 0, win_cpu_ms_ = 0, win_span_ms_ = 0;
     // Gradient statistics (overflow check + norm), one AH_STATS_FLOATS slot per block group:
     // slot 0 = embedding / positions / final LN, slot i = block i. Each slot is zeroed and filled
