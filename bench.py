@@ -488,10 +488,12 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
         "h2d_gbps": st_t["h2d_gbps"], "d2h_gbps": st_t["d2h_gbps"],
         "pinned_copy_peak_gbps": [prof["h2d_bw"] / 1e9, prof["d2h_bw"] / 1e9],
         "window_iters": st_t["window_iters"],
+        "stream_chunks": st_t["stream_chunks"],
         "definition": "hidden = 1 - copy_blocked / (H2D + D2H busy). copy_blocked = compute-stream idle time "
-                      "before an op that depends on a prefetch, while that copy was running; cpu_optim_blocked = "
-                      "the idle time before the copy started (it waited for CpuOptim / the copy lane's order). "
-                      "CUDA-event timestamps over the last drained iterations of the timed region",
+                      "before an op that depends on a prefetch, while that copy was running (for a prefetch "
+                      "streamed in chunks behind the host AdamW: while its last chunk was copied); "
+                      "cpu_optim_blocked = the rest of the idle time (the copy waited for CpuOptim / the copy "
+                      "lane's order). CUDA-event timestamps over the last drained iterations of the timed region",
     }
     burst = bound_by != "compute"
     bf16_peak, hbm_peak, peak_kind = peaks(burst)
