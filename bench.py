@@ -409,12 +409,16 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
 
     # ---- timed region: K iterations, inputs resident in HBM
     L0 = N.lib().ah_kernel_launches()
+    rsv0 = tr.stats()["pool_reserved_bytes"]
     tr.reset_stats()
     with ClockSampler(local) as clocks:
         ms_max = timed(steps)
     launches = N.lib().ah_kernel_launches() - L0
     st_t = tr.stats()  # lanes over the timed region; offload window = its last iterations
     loss = tr.drain()
+    # iteration spans of the last drained iterations (compute-stream start of F_1 to the next one)
+    f1 = sorted(e["ts"] for e in tr.trace() if e["name"] == "F_1" and e["cat"] == "COMPUTE")
+    iter_ms = [(b - a) / 1e3 for a, b in zip(f1, f1[1:])]
     _, mem_peak = tr.memory_csv()  # measured timeline of the window (reference CSV schema)
     cal = tr.calibrate()  # the window's in-step block durations in the reference cost model
     value = T * steps * world / (ms_max / 1e3)
@@ -549,6 +553,11 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
                                 "them"},
         "memory": {"measured_peak_gib": mem_peak / 2**30, "simulated_peak_gib": st["simulated_peak_bytes"] / 2**30,
                    "eq1_gib": st["modeled_peak_bytes"] / 2**30,
+                   "pool_reserved_gib": [rsv0 / 2**30, st_t["pool_reserved_bytes"] / 2**30],
+                   "compute_enqueue_ms_per_step": st_t["compute_enqueue_ms"] / steps,
+                   "compute_enqueue_max_ms": st_t["compute_enqueue_max_ms"],
+                   "window_iter_ms": iter_ms,
+                   "buffer_overflows": st_t["buffer_overflows"],
                    "source": "Trainer.memory_csv(): persistent + stream-ordered transient buffers at op start / end"},
         "ps_gain": ps_gain,
         "grad": {"norm": st_t["grad_norm"], "nonfinite": st_t["nonfinite_grads"],

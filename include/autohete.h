@@ -286,6 +286,16 @@ typedef struct ah_trainer_stats {
      * per block vector (1 = whole-block ops; env AH_STREAM_CHUNK_MB sets the chunk size, 16 MB
      * of bf16 by default, 0 = off) */
     int32_t stream_chunks;
+    /* the stream-ordered pool's physically reserved bytes now (it grows when a transient
+     * allocation pattern outruns the reservation made at create) */
+    int64_t pool_reserved_bytes;
+    /* host time the compute lane thread spent enqueueing compute ops since the last reset (sum,
+     * max over ops): a stalled enqueue (CPU starvation, a pool growth in cudaMallocAsync) leaves
+     * the GPU idle inside an op */
+    double compute_enqueue_ms, compute_enqueue_max_ms;
+    /* block weight / gradient buffers served by the stream-ordered pool because every slot of the
+     * fixed buffer arena (sized by the simulated transient peak) was live (expected 0) */
+    int32_t buffer_overflows;
 } ah_trainer_stats;
 
 int ah_trainer_create(const ah_trainer_config* cfg, void** trainer);

@@ -151,7 +151,9 @@ class TrainerStats(C.Structure):
         ("window_ms", C.c_double), ("sim_steady_fifo_s", C.c_double), ("sim_steady_ps_s", C.c_double),
         ("priority_sched", C.c_int32), ("grad_norm", C.c_double), ("nonfinite_grads", C.c_int64),
         ("skipped_updates", C.c_int32), ("sim_lane_busy_ms", C.c_double * 4),
-        ("stream_chunks", C.c_int32),
+        ("stream_chunks", C.c_int32), ("pool_reserved_bytes", C.c_int64),
+        ("compute_enqueue_ms", C.c_double), ("compute_enqueue_max_ms", C.c_double),
+        ("buffer_overflows", C.c_int32),
     ]
 
 

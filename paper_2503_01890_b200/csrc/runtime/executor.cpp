@@ -153,10 +153,13 @@ Trainer::~Trainer() {
             cudaFree(b.m1);
             cudaFree(b.m2);
         }
-        if (b.wbuf) cudaFree(b.wbuf);
-        if (b.acts) cudaFree(b.acts);
+
     }
     for (uint16_t* x : x_) cudaFree(x);
+    if (acts_arena_) cudaFree(acts_arena_);
+    for (uint16_t* p : wslot_ptr_) cudaFree(p);
+    for (cudaEvent_t e : wslot_ev_)
+        if (e) cudaEventDestroy(e);
     for (void* p : {(void*)gx_[0], (void*)gx_[1], ws_mem_, (void*)wte_, (void*)wte_m_, (void*)wte_v_, (void*)wpe_,
                     (void*)wpe_m_, (void*)wpe_v_, (void*)lnf_, (void*)lnf_m_, (void*)lnf_v_, (void*)wte_b_,
                     (void*)wpe_b_, (void*)lnf_b_, (void*)dwte_, (void*)dwpe_, (void*)dwte_b_, (void*)dwpe_b_,
@@ -517,6 +520,40 @@ void Trainer::allocate_and_init() {
     check(launch_cast_f32_bf16(lnf_, lnf_b_, 2 * h, st), "cast");
     check(cudaStreamSynchronize(st), "sync");
     static_bytes_ = stat;
+    // Activation arena: the L - c_hat + 1 activation sets Eq.(1) counts (2 m_a (L - c_hat + 1)),
+    // allocated once. Activations are the largest transient buffers; taking them from the
+    // stream-ordered pool let cudaMallocAsync block the compute lane thread for up to ~2 s while
+    // the pool waited on frees pending on the copy streams (measured inside the 10B step).
+    // Slots are taken and returned on the compute stream only, so stream order makes reuse safe;
+    // the memory timeline still counts a slot from its op's start to its release.
+    {
+        const size_t sets = (size_t)std::max(1, d_.L - strategy_.c_hat + 1);
+        acts_slot_ = round_up(BlockActs::bytes(d_), 4096);
+        check(cudaMalloc(&acts_arena_, sets * acts_slot_), "activation arena");
+        for (size_t k = sets; k-- > 0;) acts_free_.push_back(static_cast<char*>(acts_arena_) + k * acts_slot_);
+    }
+    // Weight / gradient buffers (materialised, prefetched, gathered bf16 block vectors) come from a
+    // fixed set of slots: Eq.(1)'s L - p_hat + 1 resident block buffers plus the prefetch lookahead
+    // and two in-flight gradients (at least the simulated transient peak). They are taken and
+    // released on different streams (compute, side, H2D; compute, D2H), so a release records an
+    // event on its stream and the next taker's stream waits on it (GPU-side; the host never
+    // blocks). The stream-ordered pool did the same reuse with host-blocking allocations and grew
+    // by up to 10 GiB inside the timed region at 10B. Should every slot be live, one more is added
+    // with cudaMalloc (warm-up only in practice; counted in stats.buffer_overflows).
+    {
+        const int64_t arena = (int64_t)(acts_free_.size() * acts_slot_);
+        const int64_t transient = std::max<int64_t>(0, sim_.peak_gpu - (int64_t)static_bytes_ - arena);
+        wslot_bytes_ = round_up(full_len() * 2, 4096);
+        int la = 1;
+        for (int x : strategy_.prefetch_lookahead) la = std::max(la, x);
+        const size_t by_sim = (size_t)((transient + (int64_t)wslot_bytes_ - 1) / (int64_t)wslot_bytes_);
+        const size_t by_eq1 = (size_t)std::max(0, d_.L - strategy_.p_hat + 1) + (size_t)la + 2;
+        // within the GPU budget (the rest, if the schedule ever needs it, is added in warm-up)
+        const int64_t room = hw_.gpu_mem - (int64_t)static_bytes_ - arena;
+        const size_t cap = room > 0 ? (size_t)(room / (int64_t)wslot_bytes_) : 0;
+        const size_t n = std::min(by_eq1, std::max(by_sim, cap));
+        for (size_t k = 0; k < n; ++k) wslot_add();
+    }
     reserve_pool();
 }
 
@@ -524,12 +561,47 @@ void Trainer::allocate_and_init() {
 // simulated (activations, materialised / prefetched weights, gradients): the pool never
 // releases memory (release threshold = max), so the first deeply pipelined iterations do not
 // pay the driver's physical-allocation path inside the timed region.
+uint16_t* Trainer::wslot_alloc(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(wslot_mu_);
+    if (wslot_free_.empty()) {  // every slot live: one more (cudaMalloc synchronises the device)
+        wslot_add();
+        ++wslot_overflow_;
+    }
+    const int k = wslot_free_.front();  // the longest-released slot
+    wslot_free_.pop_front();
+    if (wslot_recorded_[(size_t)k]) check(cudaStreamWaitEvent(st, wslot_ev_[(size_t)k], 0), "slot reuse wait");
+    return wslot_ptr_[(size_t)k];
+}
+
+void Trainer::wslot_add() {
+    void* p = nullptr;
+    check(cudaMalloc(&p, wslot_bytes_), "block buffer slot");
+    cudaEvent_t e = nullptr;
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    wslot_index_[p] = (int)wslot_ptr_.size();
+    wslot_ptr_.push_back(static_cast<uint16_t*>(p));
+    wslot_ev_.push_back(e);
+    wslot_recorded_.push_back(0);
+    wslot_free_.push_back((int)wslot_ptr_.size() - 1);
+}
+
+void Trainer::wslot_free(uint16_t* p, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(wslot_mu_);
+    const auto f = wslot_index_.find(p);
+    if (f == wslot_index_.end()) throw std::logic_error("executor: release of an unknown block buffer");
+    const int k = f->second;
+    check(cudaEventRecord(wslot_ev_[(size_t)k], st), "slot release");
+    wslot_recorded_[(size_t)k] = 1;
+    wslot_free_.push_back(k);
+}
+
 void Trainer::reserve_pool() {
     size_t free_b = 0, total_b = 0;
     check(cudaMemGetInfo(&free_b, &total_b), "mem info");
-    const int64_t transient = std::max<int64_t>(0, sim_.peak_gpu - (int64_t)static_bytes_);
+    // activations and weight buffers come from the fixed arenas: the pool only backs an
+    // overflow weight buffer (never expected) — keep two buffers' worth warm
+    size_t want = 2 * full_len() * 2;
     const size_t headroom = (size_t)1 << 30;
-    size_t want = (size_t)transient + (transient ? headroom : 0);
     if (want + headroom > free_b) want = free_b > 2 * headroom ? free_b - 2 * headroom : 0;
     if (want == 0) return;
     void* p = nullptr;
@@ -672,8 +744,13 @@ void Trainer::lane_main(int lane) {
                 }
                 cv_.notify_all();
                 if (lane == kCompute) {
+                    const auto h0 = Clock::now();
                     prefetch_weights(*it, idx, op);  // the next op's weights, overlapping this op
                     run_compute(*it, op);
+                    const double hm = std::chrono::duration<double, std::milli>(Clock::now() - h0).count();
+                    std::lock_guard<std::mutex> lk(mu_);
+                    enqueue_ms_ += hm;
+                    enqueue_max_ms_ = std::max(enqueue_max_ms_, hm);
                 }
                 else if (lane == kH2D)
                     run_h2d(*it, op);
@@ -805,7 +882,7 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
     const size_t mp = d_.m_p();
     const size_t off = shard_ * (size_t)dp_rank_;
     auto materialize = [&]() {  // bf16 weights from the on-GPU fp32 master (footnote 2)
-        check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, st), "alloc wbuf");
+        b.wbuf = wslot_alloc(st);
         op.alloc_b += (int64_t)full_len() * 2;
         if (dp_) {  // own shard, then all-gather the others over NVLink (side stream)
             check(launch_cast_f32_bf16(b.master, b.wbuf + off, shard_, st), "cast");
@@ -826,17 +903,19 @@ void Trainer::run_compute(Iter& it, RtOp& op) {
         compute_after_side();
         b.needs_gather = false;
     }
-    auto alloc_acts = [&]() {
-        check(cudaMallocAsync(&b.acts, BlockActs::bytes(d_), st), "alloc acts");
+    auto alloc_acts = [&]() {  // a slot of the activation arena (allocated and freed on this stream only)
+        if (acts_free_.empty()) throw std::logic_error("executor: more live activation sets than L - c_hat + 1");
+        b.acts = acts_free_.back();
+        acts_free_.pop_back();
         op.alloc_b += (int64_t)BlockActs::bytes(d_);
     };
     auto free_acts = [&]() {
-        check(cudaFreeAsync(b.acts, st), "free acts");
+        acts_free_.push_back(b.acts);
         b.acts = nullptr;
         op.free_b += (int64_t)BlockActs::bytes(d_);
     };
     auto free_wbuf = [&]() {
-        check(cudaFreeAsync(b.wbuf, st), "free wbuf");
+        wslot_free(b.wbuf, st);
         b.wbuf = nullptr;
         op.free_b += (int64_t)full_len() * 2;
     };
@@ -904,7 +983,7 @@ void Trainer::run_h2d(Iter& it, RtOp& op) {
     const size_t mp = d_.m_p();
     const size_t n = dp_ ? shard_ : mp;  // DP: only this rank's shard crosses the host link
     uint16_t* dst = nullptr;
-    check(cudaMallocAsync((void**)&dst, full_len() * 2, s_h2d_), "alloc prefetch");
+    dst = wslot_alloc(s_h2d_);
     op.alloc_b += (int64_t)full_len() * 2;
     uint16_t* mine = dp_ ? dst + shard_ * (size_t)dp_rank_ : dst;
     if (b.o && op.streamed) {  // chunk c goes up as soon as the host AdamW finished it
@@ -943,7 +1022,7 @@ void Trainer::run_d2h(Iter& it, RtOp& op) {
     } else {
         check(cudaMemcpyAsync(b.host_bf16, src, n * 2, cudaMemcpyDeviceToHost, s_d2h_), "offload");
     }
-    check(cudaFreeAsync(b.wbuf, s_d2h_), "free after offload");
+    wslot_free(b.wbuf, s_d2h_);
     b.wbuf = nullptr;
     op.free_b += (int64_t)full_len() * 2;
 }
@@ -1067,7 +1146,7 @@ void Trainer::prefetch_weights(const Iter& it, size_t idx, RtOp& cur) {
     BlockState& b = blocks_[(size_t)y.block];
     if (b.o || b.p || b.wbuf || b.mat_pending) return;
     side_after_compute();  // the master is final: every compute op enqueued so far precedes the cast
-    check(cudaMallocAsync((void**)&b.wbuf, full_len() * 2, s_side_), "alloc wbuf");
+    b.wbuf = wslot_alloc(s_side_);
     cur.alloc_b += (int64_t)full_len() * 2;  // lives from the current op on
     if (dp_) {
         check(launch_cast_f32_bf16(b.master, b.wbuf + shard_ * (size_t)dp_rank_, shard_, s_side_), "cast");
@@ -1279,6 +1358,9 @@ void Trainer::stats(ah_trainer_stats* s) {
     uint64_t hw = 0;
     cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &hw);
     s->pool_peak_bytes = (int64_t)hw;
+    uint64_t rsv = 0;
+    cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemCurrent, &rsv);
+    s->pool_reserved_bytes = (int64_t)rsv;
     s->static_bytes = (int64_t)static_bytes_;
     s->sim_steady_s = sim_.steady_state_time;
     std::lock_guard<std::mutex> lk(mu_);
@@ -1286,6 +1368,12 @@ void Trainer::stats(ah_trainer_stats* s) {
         s->lane_busy_ms[l] = lane_stats_[l].busy_ms;
         s->lane_ops[l] = lane_stats_[l].ops;
     }
+    s->compute_enqueue_ms = enqueue_ms_;
+    {
+        std::lock_guard<std::mutex> lk2(wslot_mu_);
+        s->buffer_overflows = wslot_overflow_;
+    }
+    s->compute_enqueue_max_ms = enqueue_max_ms_;
     const int64_t per_block = dp_ ? (int64_t)shard_ : profile_.block.m_p;  // host-link elements
     // host-link bytes: every O block's forward prefetch, plus the backward re-fetch of the P blocks
     // that are also O (a P block outside O re-materialises from its GPU master, no PCIe)
@@ -1593,6 +1681,7 @@ float Trainer::timer(bool stop) {
 void Trainer::reset_stats() {
     std::lock_guard<std::mutex> lk(mu_);
     for (LaneStats& l : lane_stats_) l = LaneStats{};
+    enqueue_ms_ = enqueue_max_ms_ = 0.0;
     win_iters_ = win_compute_ms_ = win_h2d_ms_ = win_d2h_ms_ = win_blocked_ms_ = 0;
     win_h2d_bytes_ = win_d2h_bytes_ = win_h2d_link_ms_ = 0;
     win_copy_blocked_ms_ = win_upstream_blocked_ms_ = win_cpu_ms_ = win_span_ms_ = 0;

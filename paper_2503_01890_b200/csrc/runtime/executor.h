@@ -214,6 +214,21 @@ private:
     std::vector<uint16_t*> x_;        // residual stream x[0..L] (x[0] = embedding output)
     uint16_t* gx_[2] = {nullptr, nullptr};  // residual-gradient ping-pong
     void* ws_mem_ = nullptr;
+    void* acts_arena_ = nullptr;      // L - c_hat + 1 activation sets (see allocate_and_init)
+    size_t acts_slot_ = 0;
+    std::vector<void*> acts_free_;    // free slots, LIFO; compute lane only
+    // block weight / gradient buffer slots (see allocate_and_init)
+    size_t wslot_bytes_ = 0;
+    std::vector<uint16_t*> wslot_ptr_;
+    std::map<const void*, int> wslot_index_;
+    std::vector<cudaEvent_t> wslot_ev_;   // recorded on the releasing stream
+    std::vector<uint8_t> wslot_recorded_;
+    std::deque<int> wslot_free_;
+    std::mutex wslot_mu_;
+    int wslot_overflow_ = 0;
+    uint16_t* wslot_alloc(cudaStream_t st);
+    void wslot_add();  // caller holds wslot_mu_ (or is the constructor)
+    void wslot_free(uint16_t* p, cudaStream_t st);
     Workspace ws_;
     // head / embedding (GPU-resident, m_gc)
     float *wte_ = nullptr, *wte_m_ = nullptr, *wte_v_ = nullptr;
@@ -245,6 +260,7 @@ private:
     std::thread lanes_[4];
     size_t lane_pos_[4] = {0, 0, 0, 0};  // index into iters_ window per lane
     LaneStats lane_stats_[4];
+    double enqueue_ms_ = 0.0, enqueue_max_ms_ = 0.0;  // compute lane: host time per compute op enqueue
     float last_loss_ = 0.f;
     // offload-overlap accounting of the last drain (see ah_trainer_stats)
     double win_iters_ = 0, win_compute_ms_ = 0, win_h2d_ms_ = 0, win_d2h_ms_ = 0, win_blocked_ms_ = 0;
