@@ -417,7 +417,11 @@ def run_workload(a, cfg_name, budget_gib, steps, warmup, rank, world, local, dis
     st_t = tr.stats()  # lanes over the timed region; offload window = its last iterations
     loss = tr.drain()
     # iteration spans of the last drained iterations (compute-stream start of F_1 to the next one)
-    f1 = sorted(e["ts"] for e in tr.trace() if e["name"] == "F_1" and e["cat"] == "COMPUTE")
+    trace = tr.trace()  # real run, reference Chrome-trace schema (all four lanes)
+    if os.environ.get("AH_BENCH_TRACE") and headline:
+        with open(os.environ["AH_BENCH_TRACE"], "w") as f:
+            json.dump(trace, f)
+    f1 = sorted(e["ts"] for e in trace if e["name"] == "F_1" and e["cat"] == "COMPUTE")
     iter_ms = [(b - a) / 1e3 for a, b in zip(f1, f1[1:])]
     _, mem_peak = tr.memory_csv()  # measured timeline of the window (reference CSV schema)
     cal = tr.calibrate()  # the window's in-step block durations in the reference cost model

@@ -114,6 +114,7 @@ Trainer::Trainer(const ah_trainer_config& cfg) {
     check(cudaStreamCreateWithPriority(&s_h2d_, cudaStreamNonBlocking, lo), "stream");
     check(cudaStreamCreateWithPriority(&s_d2h_, cudaStreamNonBlocking, lo), "stream");
     check(cudaStreamCreateWithPriority(&s_side_, cudaStreamNonBlocking, hi), "stream");
+    check(cudaStreamCreateWithFlags(&s_mark_, cudaStreamNonBlocking), "stream");
     check(cudaEventCreateWithFlags(&ev_c2s_, cudaEventDisableTiming), "event");
     check(cudaEventCreateWithFlags(&ev_s2c_, cudaEventDisableTiming), "event");
     check(cudaGetDevice(&device_), "get device");
@@ -179,6 +180,7 @@ Trainer::~Trainer() {
         for (cudaEvent_t e : b.go_ev) cudaEventDestroy(e);
     }
     cudaStreamDestroy(s_d2h_);
+    cudaStreamDestroy(s_mark_);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -644,10 +646,10 @@ void Trainer::build_iteration(Iter& it) {
                 }
         check(cudaEventCreateWithFlags(&r.done_ev, cudaEventDisableTiming), "event");
         check(cudaEventCreateWithFlags(&r.start_ev, cudaEventDisableTiming), "event");
-        if (r.lane != kCpu) {
-            check(cudaEventCreate(&r.t0), "event");
-            check(cudaEventCreate(&r.t1), "event");
-        }
+        // GPU lanes: timing events on the op's stream; CPU lane: on the idle marker stream, where a
+        // record completes at once, so the host AdamW ops land on the same timeline (trace)
+        check(cudaEventCreate(&r.t0), "event");
+        check(cudaEventCreate(&r.t1), "event");
         it.ops.emplace(OpKey{(int)so.kind, so.block, so.backward_copy}, std::move(r));
     }
     for (int l = 0; l < 4; ++l) it.lane_order[l] = order_[ksim - 1][l];
@@ -725,7 +727,9 @@ void Trainer::lane_main(int lane) {
                         op.state = 1;
                     }
                     cv_.notify_all();
+                    check(cudaEventRecord(op.t0, s_mark_), "record");
                     run_cpu(*it, op);
+                    check(cudaEventRecord(op.t1, s_mark_), "record");
                     {
                         std::lock_guard<std::mutex> lk(mu_);
                         op.state = 3;
@@ -1414,7 +1418,7 @@ std::string Trainer::trace_json() {
     for (Iter* it : iters_)
         for (auto& kv : it->ops) {
             RtOp& o = kv.second;
-            if (o.lane == kCpu || !origin) continue;
+            if (!origin) continue;
             float a = 0, b = 0;
             if (cudaEventElapsedTime(&a, origin, o.t0) != cudaSuccess) continue;
             if (cudaEventElapsedTime(&b, origin, o.t1) != cudaSuccess) continue;

@@ -209,6 +209,7 @@ private:
 
     cudaStream_t s_compute_ = nullptr, s_h2d_ = nullptr, s_d2h_ = nullptr;
     cudaStream_t s_side_ = nullptr;
+    cudaStream_t s_mark_ = nullptr;  // idle: timestamps of host (CpuOptim) ops on the GPU timeline
     cudaEvent_t ev_c2s_ = nullptr, ev_s2c_ = nullptr;  // reused: a wait binds to the latest record
     std::vector<BlockState> blocks_;  // index 1..L
     std::vector<uint16_t*> x_;        // residual stream x[0..L] (x[0] = embedding output)

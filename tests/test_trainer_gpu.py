@@ -124,7 +124,7 @@ def test_realised_lane_order_matches_scheduler(cuda_device, native):
     tr.drain()
     sched = tr.schedule()  # steady-state per-lane order from hetsim::run
     trace = tr.trace()
-    for lane in ("COMPUTE", "H2D", "D2H"):
+    for lane in ("COMPUTE", "H2D", "D2H", "CPU"):  # host AdamW ops are on the trace timeline too
         want = [t.split(":")[1].rstrip("b") for t in sched if t.startswith(lane + ":")]
         got = [e["name"] for e in trace if e["cat"] == lane]
         # every realised iteration (window) repeats the simulated lane order
