@@ -553,7 +553,8 @@ void Trainer::allocate_and_init() {
         // within the GPU budget (the rest, if the schedule ever needs it, is added in warm-up)
         const int64_t room = hw_.gpu_mem - (int64_t)static_bytes_ - arena;
         const size_t cap = room > 0 ? (size_t)(room / (int64_t)wslot_bytes_) : 0;
-        const size_t n = std::min(by_eq1, std::max(by_sim, cap));
+        size_t n = std::min(by_eq1, std::max(by_sim, cap));
+        if (const char* e = std::getenv("AH_BUFFER_SLOTS")) n = (size_t)std::max(1, std::atoi(e));  // tests
         for (size_t k = 0; k < n; ++k) wslot_add();
     }
     reserve_pool();

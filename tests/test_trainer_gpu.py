@@ -114,6 +114,19 @@ def test_streamed_offload_chain_is_bit_identical(cuda_device, native, monkeypatc
     assert st["stream_chunks"] == 1
 
 
+def test_block_buffer_slots_grow_on_demand(cuda_device, native, monkeypatch):
+    """Starting from a single block-buffer slot, the executor adds slots as the schedule needs them
+    (event-ordered reuse across the compute / side / H2D / D2H streams) and trains bit-identically."""
+    base_loss, base_state, _ = run_plan(PLANS[0])
+    monkeypatch.setenv("AH_BUFFER_SLOTS", "1")
+    for plan in (PLANS[2], PLANS[4]):
+        loss, state, st = run_plan(plan)
+        assert st["buffer_overflows"] > 0
+        assert loss == base_loss, plan
+        for a, b in zip(state, base_state):
+            assert np.array_equal(a.view(np.uint32), b.view(np.uint32)), plan
+
+
 def test_realised_lane_order_matches_scheduler(cuda_device, native):
     from paper_2503_01890_b200.trainer import PlanConfig
     tr = make(plan=PlanConfig(c_hat=2, p_hat=2, o_hat=4, priority_sched=True, fine_tune=False,
