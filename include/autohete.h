@@ -252,7 +252,8 @@ typedef struct ah_trainer_stats {
     int64_t m_p, m_gc;            /* per-block params, constant GPU residue (bytes) */
     int64_t modeled_peak_bytes;   /* Eq.(1) for the chosen strategy */
     int64_t simulated_peak_bytes; /* hetsim::run peak */
-    int64_t pool_peak_bytes;      /* measured: stream-ordered pool high watermark */
+    int64_t pool_peak_bytes;      /* measured: default stream-ordered pool high watermark (the executor's
+                                   * transient buffers come from its fixed arenas: ~0) */
     int64_t static_bytes;         /* measured: persistent device allocations */
     double sim_steady_s;          /* hetsim::run steady-state iteration time */
     double lane_busy_ms[4];       /* compute, h2d, d2h, cpu: summed op time since reset */

@@ -107,12 +107,12 @@ def build(force: bool = False, jobs: int = 0, verbose: bool = False) -> dict:
     dp_objs = [j[1] for j in work if j[0] == "dp"]
     core_so = os.path.join(LIB, "libhetsim_core.so")
     if force or _stale(core_so, core_objs, 0.0):
-        _run(["g++", "-shared", "-o", core_so, *core_objs])
+        _run(["g++", "-shared", "-Wl,--no-undefined", "-o", core_so, *core_objs])
     dp_so = os.path.join(LIB, "libautohete.so")
     if force or _stale(dp_so, dp_objs + [core_so], 0.0):
         nccl_lib = os.path.join(NCCL_HOME, "lib")
         link = [NVCC, *ARCH, "-shared", "-o", dp_so, *dp_objs, "-L" + LIB, "-lhetsim_core",
-                "-Xlinker", "-rpath=$ORIGIN", "-Xcompiler", "-fopenmp", "-lgomp"]
+                "-Xlinker", "-rpath=$ORIGIN", "-Xlinker", "--no-undefined", "-Xcompiler", "-fopenmp", "-lgomp"]
         if os.path.exists(os.path.join(nccl_lib, "libnccl.so.2")):
             link += ["-L" + nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib]
         _run(link)

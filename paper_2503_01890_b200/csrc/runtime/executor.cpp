@@ -557,13 +557,9 @@ void Trainer::allocate_and_init() {
         if (const char* e = std::getenv("AH_BUFFER_SLOTS")) n = (size_t)std::max(1, std::atoi(e));  // tests
         for (size_t k = 0; k < n; ++k) wslot_add();
     }
-    reserve_pool();
 }
 
-// Grow the stream-ordered pool once, up front, to the transient footprint the scheduler
-// simulated (activations, materialised / prefetched weights, gradients): the pool never
-// releases memory (release threshold = max), so the first deeply pipelined iterations do not
-// pay the driver's physical-allocation path inside the timed region.
+
 uint16_t* Trainer::wslot_alloc(cudaStream_t st) {
     std::lock_guard<std::mutex> lk(wslot_mu_);
     if (wslot_free_.empty()) {  // every slot live: one more (cudaMalloc synchronises the device)
@@ -596,24 +592,6 @@ void Trainer::wslot_free(uint16_t* p, cudaStream_t st) {
     check(cudaEventRecord(wslot_ev_[(size_t)k], st), "slot release");
     wslot_recorded_[(size_t)k] = 1;
     wslot_free_.push_back(k);
-}
-
-void Trainer::reserve_pool() {
-    size_t free_b = 0, total_b = 0;
-    check(cudaMemGetInfo(&free_b, &total_b), "mem info");
-    // activations and weight buffers come from the fixed arenas: the pool only backs an
-    // overflow weight buffer (never expected) — keep two buffers' worth warm
-    size_t want = 2 * full_len() * 2;
-    const size_t headroom = (size_t)1 << 30;
-    if (want + headroom > free_b) want = free_b > 2 * headroom ? free_b - 2 * headroom : 0;
-    if (want == 0) return;
-    void* p = nullptr;
-    if (cudaMallocAsync(&p, want, s_compute_) != cudaSuccess) {
-        cudaGetLastError();
-        return;  // best effort
-    }
-    check(cudaFreeAsync(p, s_compute_), "pool reserve free");
-    check(cudaStreamSynchronize(s_compute_), "pool reserve sync");
 }
 
 // ---------------------------------------------------------------------------------------

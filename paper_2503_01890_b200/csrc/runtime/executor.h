@@ -115,7 +115,7 @@ private:
         int state = 0;  // 0 pending, 1 started (start_ev recorded), 2 issued (done_ev recorded), 3 done (host)
         double host_ms = 0.0;
         bool done_on_side = false;  // DP backward: done_ev follows the gradient reduce-scatter on s_side_
-        int64_t alloc_b = 0, free_b = 0;  // stream-ordered pool bytes taken at its start / returned at its end
+        int64_t alloc_b = 0, free_b = 0;  // transient bytes (arena slots) taken at its start / returned at its end
         // Sub-block streaming (nsub_ > 1). CpuOptim: chunks of the block updated so far (the
         // next iteration's forward ParamPrefetch copies chunk c up as soon as progress > c).
         // Streamed ParamPrefetch: the CpuOptim it follows, and per-chunk copy timing events
@@ -150,7 +150,6 @@ private:
 
     void plan(const ah_trainer_config& cfg);
     void allocate_and_init();
-    void reserve_pool();
     void build_iteration(Iter& it);
     void lane_main(int lane);
     // state_only > 0: wait until the dependency reached that state (1 started, 2 issued) and
