@@ -44,6 +44,8 @@ def test_product_arm_contract(cuda_device, native):
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["cpu_baseline"]["value"] and d["cpu_baseline"]["cores"] >= 1
     assert d["adam"]["roofline"]["bound"] == "hbm"
+    m = d["memory"]  # the executor's transient buffers come from its arenas: nothing allocated on the fly
+    assert m["buffer_overflows"] == 0 and m["measured_peak_gib"] <= m["eq1_gib"] * 1.1
 
 
 def test_bench_spawns_ranks():
