@@ -32,7 +32,9 @@ extern "C" {
 #define AH_ERR_INTERNAL -6  /* std::logic_error / anything else */
 
 const char* ah_last_error(void);
-int ah_abi_version(void); /* bumps on any signature change */
+int ah_abi_version(void); /* bumps on any signature or struct layout change; 5: ah_trainer_stats gained
+                           * stream_chunks, pool_reserved_bytes, compute_enqueue_ms / _max_ms,
+                           * buffer_overflows (appended) */
 
 /* ---------------------------------------------------------------------------------------
  * Optimizer (OpKind::GpuOptim / OpKind::CpuOptim).

@@ -33,6 +33,9 @@ class AdamHParams(C.Structure):
     ]
 
 
+ABI_VERSION = 5  # include/autohete.h ah_abi_version()
+
+
 def lib() -> C.CDLL:
     """Load libautohete.so (and its libhetsim_core.so dependency) exactly once."""
     global _lib
@@ -41,9 +44,13 @@ def lib() -> C.CDLL:
         if not os.path.exists(path):
             raise NativeError(f"{path} not built; run `python -m paper_2503_01890_b200.build`")
         C.CDLL(os.path.join(LIB_DIR, "libhetsim_core.so"), mode=C.RTLD_GLOBAL)
-        _lib = C.CDLL(path, mode=C.RTLD_GLOBAL)
-        _declare(_lib)
-        _declare_extra(_lib)
+        lib_ = C.CDLL(path, mode=C.RTLD_GLOBAL)
+        _declare(lib_)
+        _declare_extra(lib_)
+        got = lib_.ah_abi_version()
+        if got != ABI_VERSION:  # a stale build would read / write the structs with another layout
+            raise NativeError(f"{path}: ABI version {got}, this package expects {ABI_VERSION}; rebuild")
+        _lib = lib_
     return _lib
 
 

@@ -39,7 +39,7 @@ using ah::set_error;
 extern "C" {
 
 const char* ah_last_error(void) { return ah::g_last_error.c_str(); }
-int ah_abi_version(void) { return 4; }
+int ah_abi_version(void) { return 5; }
 
 int ah_adam_step(const ah_adam_hparams* hp, float* p, float* m, float* v, const uint16_t* g,
                  uint16_t* p_bf16, size_t n, float inv_scale, const int32_t* skip_flag,
