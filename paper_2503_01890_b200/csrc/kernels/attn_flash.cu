@@ -1,16 +1,17 @@
 // Flash-style causal attention on tcgen05 (sm_100a): the forward keeps only O and the per-row
 // log-sum-exp; the backward recomputes P from Q, K and the log-sum-exp.
 //
-// Forward (flash_fwd_pk_kernel): persistent, one CTA per SM over snake-ordered (128-query tile,
-// head, sequence) items, heavy (long causal) items first:
-//   S_j = Q K_j^T            tcgen05.mma into one of two TMEM score buffers
-//   online softmax            8 warps: thread = query row, warp pair (w, w + 4) splits the 128
-//                             keys of a tile; the pair exchanges its tile max through smem
+// Forward (flash_fwd_k64_kernel): persistent, two CTAs per SM, each walking snake-ordered
+// (128-query tile, head, sequence) items, heavy (long causal) items first:
+//   S_j = Q K_j^T            128 queries x 64 keys, tcgen05.mma into one of two TMEM score buffers
+//                             (S_{j+1} is computed while the softmax works on S_j)
+//   online softmax            4 warps, thread = query row (row_chunk: 32-key chunks, one TMEM read
+//                             per score, paired FFMA2 / FADD2, a quarter of the exponentials on the
+//                             FMA pipe)
 //   O += P_j V_j              P_j (bf16) written back into its score buffer, A read from TMEM
-// Softmax runs in the log2 domain on raw scores, p = 2^(S * scale * log2e - m * scale * log2e),
-// with lazy rescaling: the running max m only moves (and O / l are rescaled in TMEM) when the
-// tile max exceeds it by more than 2^8. Output O / l and lse2 = m * scale * log2e + log2(l) per
-// row (the backward's softmax statistics).
+// Softmax runs in the log2 domain, p = 2^(S * scale * log2e - m), with lazy rescaling: the running
+// max m only moves (and l / O / the tile's stored P chunks are rescaled) when a chunk max exceeds
+// it by more than 2^8. Output O / l and lse2 = m + log2(l) per row (the backward's statistics).
 //
 // Backward (flash_bwd_t_kernel): persistent over (128-key tile, head, sequence) items, scores
 // formed key-major so P^T and dS^T are the TMEM A operands of the dV / dK MMAs:
@@ -19,9 +20,10 @@
 //   dV += P^T dO_i, dK += dS^T Q_i                             (TMEM accumulators)
 // dS^T also goes to HBM for the deterministic dQ = dS K GEMM (no cross-CTA atomics).
 //
-// Operand staging: every tile is a K-major SWIZZLE_128B 128 x 128 bf16 box pair (two 64-column
-// atoms); read as the MN-major operand of its transpose it gives V, dO, Q for free. Warp roles:
-// 0 TMA producer, 1 MMA issuer (one thread), 2 TMEM allocator, 4.. softmax / epilogue.
+// Operand staging: every tile is a K-major SWIZZLE_128B box pair (two 64-column atoms; 128 rows,
+// 64 for the forward's K / V); read as the MN-major operand of its transpose it gives V, dO, Q for
+// free. Backward warp roles: 0 TMA producer, 1 MMA issuer (one thread), 2 TMEM allocator, 4..
+// softmax / epilogue.
 // Shapes: head_dim = 128, seq_len % 128 == 0 (others take the unfused GEMM path, gpt_model.cpp).
 #include <cuda.h>
 
@@ -74,15 +76,14 @@ struct FwdParams {
 
 
 // ---------------------------------------------------------------------------------------
-// Persistent forward (the default): one CTA per SM walks a snake-ordered list of
-// (query tile, head, sequence) items, heavy (long causal) items first, and keeps the pipeline
-// full across items: Q is double-buffered per item, the K/V ring and the two TMEM score buffers
-// continue across item boundaries, and the next item's first score tile is issued while the
-// softmax warps run the current item's epilogue. P_j (bf16) is written back by the softmax warps
-// into the first 64 columns of its own score buffer and fed to O += P_j V_j straight from TMEM
-// (tcgen05.mma A-from-TMEM), so P never touches shared memory and softmax j+1 never waits for
-// the P V MMA of tile j (the score buffer of j is only reused by S_{j+2}, which the MMA thread
-// issues after P_j V_j: tcgen05.mma executes in issue order).
+// Persistent forward pipeline: a CTA walks a snake-ordered list of (query tile, head, sequence)
+// items, heavy (long causal) items first, and keeps the pipeline full across items: the K/V ring
+// and the two TMEM score buffers continue across item boundaries, and the next item's first score
+// tile is issued while the softmax warps run the current item's epilogue. P_j (bf16) is written
+// back by the softmax warps into its own score buffer and fed to O += P_j V_j straight from TMEM
+// (tcgen05.mma A-from-TMEM), so P never touches shared memory and softmax j+1 never waits for the
+// P V MMA of tile j (the score buffer of j is only reused by S_{j+2}, which the MMA thread issues
+// after P_j V_j: tcgen05.mma executes in issue order). O += P V with A from TMEM:
 __device__ __forceinline__ void mma_f16_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
@@ -108,129 +109,243 @@ struct FwdItems {
     }
 };
 
-template <int kParts>
-__global__ void __launch_bounds__((4 + 4 * kParts) * 32, 1)
-flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                    const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams A) {
+// ---------------------------------------------------------------------------------------
+// Row-per-thread softmax of the forward: a thread owns one query row and the keys of a score
+// tile, read from TMEM in 32-key chunks (one TMEM read per score). The
+// exponentials use the running row max (lazy rescale: p <= 2^8 between rescales) while each
+// chunk's max is checked; a chunk whose max exceeds it by more than 2^8 takes the out-of-line
+// slow path (new max; l, the tile's partial sums, its stored P chunks and O rescaled). P chunk c
+// (bf16 pairs) lands in score columns [16c, 16c + 16), already read. A quarter of the
+// exponentials run on the FMA pipe (ex2_poly) and the scale / sum arithmetic is paired (FFMA2 /
+// FADD2): the loop is MUFU- and issue-bound. The chunk loop is rolled so the whole softmax code
+// stays in the instruction cache (fully unrolled variants ran chunks 2-5x slower whenever
+// warps executed different variants).
+
+// 2^x on the FMA pipe for x in [-120, 9]: x = n + f (n = round(x), |f| <= 1/2), 2^f by a degree-3
+// near-minimax polynomial (max rel. error 7.5e-5, far below the bf16 rounding of P), 2^n added to
+// the exponent field. Masked keys never take this path (they need an exact 0).
+__device__ __forceinline__ float ex2_poly(float x) {
+    x = fmaxf(x, -120.f);
+    const float t = x + 12582912.f;  // 1.5 * 2^23: round(x) in the low mantissa bits
+    const float f = x - (t - 12582912.f);
+    float p = fmaf(0.05517052f, f, 0.24260917f);
+    p = fmaf(p, f, 0.69326102f);
+    p = fmaf(p, f, 0.9999282f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t x[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]), "=r"(x[8]),
+          "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(x[i]);
+}
+
+// Slow path (rare): P chunks [0, c) of this tile and O times alpha. O must hold every P V issued
+// for this item: the one of the previous tile may still run (S_{j+1} is issued before P_j V_j).
+__device__ __noinline__ void row_rescale(float alpha, int c, uint32_t sbuf, uint32_t obuf, int j, uint32_t pv_bar,
+                                         uint32_t g) {
+#pragma unroll 1
+    for (int cc = 0; cc < c; ++cc) {
+        float pw[16];
+        ld16(sbuf + cc * 16, pw);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const uint32_t u = __float_as_uint(pw[i]);
+            pw[i] = __uint_as_float(pack_bf16x2_rn(__uint_as_float(u << 16) * alpha, __uint_as_float(u & 0xffff0000u) * alpha));
+        }
+        st16(sbuf + cc * 16, pw);
+    }
+    if (j > 0) {
+        mbar_wait(pv_bar, (g - 1) & 1);
+        fence_after();
+#pragma unroll 1
+        for (int cc = 0; cc < 4; ++cc) {
+            float o[32];
+            ld32(obuf + cc * 32, o);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            st32(obuf + cc * 32, o);
+        }
+    }
+}
+
+// kMask: the diagonal chunk (keys > row masked to an exact 0); kPoly: ex2 of a quarter on the FMA pipe.
+template <bool kMask, bool kPoly>
+__device__ __forceinline__ void row_chunk(int c, uint32_t sbuf, uint32_t obuf, int lane, int j, uint32_t g, float sl2,
+                                          float& mb, float& l, unsigned long long (&ad2)[2], uint32_t pv_bar) {
+    float v[32];
+    ld32(sbuf + c * 32, v);
+    float cm[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        if (kMask && i > lane) v[i] = -INFINITY;
+        cm[i & 3] = fmaxf(cm[i & 3], v[i]);
+    }
+    const float ym = fmaxf(fmaxf(cm[0], cm[1]), fmaxf(cm[2], cm[3])) * sl2;  // chunk max, scaled
+    if (mb == -INFINITY) mb = ym;  // the item's first chunk (key 0 <= q: finite)
+    const bool up = ym - mb > kRescaleLog2;
+    if (__any_sync(0xffffffffu, up)) {
+        const float alpha = up ? ex2_approx(mb - ym) : 1.f;
+        row_rescale(alpha, c, sbuf, obuf, j, pv_bar, g);
+        if (up) mb = ym;
+        l *= alpha;
+        const unsigned long long a2 = f2pack(alpha, alpha);
+        ad2[0] = fmul2(ad2[0], a2);
+        ad2[1] = fmul2(ad2[1], a2);
+    }
+    const unsigned long long s2 = f2pack(sl2, sl2), nb2 = f2pack(-mb, -mb);
+    float pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        float x0, x1;
+        f2unpack(ffma2(f2pack(v[2 * i], v[2 * i + 1]), s2, nb2), x0, x1);
+        const bool poly = kPoly && (i & 3) == 3;
+        const float p0 = poly ? ex2_poly(x0) : ex2_approx(x0), p1 = poly ? ex2_poly(x1) : ex2_approx(x1);
+        ad2[i & 1] = fadd2(ad2[i & 1], f2pack(p0, p1));
+        pk[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
+    }
+    st16(sbuf + c * 16, pk);
+}
+
+// ---------------------------------------------------------------------------------------
+// Forward with 64-key score tiles, two CTAs per SM. Each CTA is a single-query-tile pipeline
+// (persistent over snake-ordered items, S double-buffered ahead of P V), a score tile is 128 queries x 64 keys, so a CTA needs
+// only 256 TMEM columns (S double-buffered: 0-63, 64-127; O: 128-255) and ~106 KB of shared
+// memory, and two CTAs share every SM. The softmax is row-per-thread (row_chunk: one TMEM read
+// per score, lazy max, paired arithmetic, a quarter of the exponentials on the FMA pipe) with 4
+// warps per CTA, so each SM sub-partition runs two independent softmax warps (one per CTA)
+// while the tensor pipe serves both CTAs: one warp alone cannot hide its own TMEM / MUFU
+// latencies (a row-per-thread 128-key variant with one CTA per SM measured 54.7 us; the previous
+// forward, two warps per row exchanging the row max through shared memory, 51.4 us; this one 48.7).
+constexpr int kKT = 64;                                  // keys per score tile
+constexpr uint32_t kTileKV = kKT * kHD * 2;             // 16 KB: two 64-column SWIZZLE_128B atoms
+__device__ __forceinline__ uint64_t kdesc_kv(uint32_t base, int t) {  // K (64 rows) as K-major B
+    return sdesc(base + (t >> 2) * (kTileKV / 2) + (t & 3) * 32, 16, 1024);
+}
+__device__ __forceinline__ uint64_t mndesc_kv(uint32_t base, int t) {  // V (64 rows) as MN-major B, K step t
+    return sdesc(base + t * 2048, kTileKV / 2, 1024);
+}
+__device__ __forceinline__ void load_kv(uint32_t dst, const CUtensorMap* m, uint32_t bar, int row, int head, int b) {
+    tma_load_4d(dst, m, bar, 0, row, head, b);
+    tma_load_4d(dst + kTileKV / 2, m, bar, 64, row, head, b);
+}
+
+__global__ void __launch_bounds__(192, 2)
+flash_fwd_k64_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                     const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmO, const FwdParams A) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = align1024(smem_raw);
-    uint8_t* sQ = sm;              // [2] per item
-    uint8_t* sK = sm + 2 * kTile;  // [2]
-    uint8_t* sV = sm + 4 * kTile;  // [2]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 6 * kTile);
-    uint64_t* q_full = bar;        // [2]
-    uint64_t* q_empty = bar + 2;   // [2]
-    uint64_t* k_full = bar + 4;    // [2]
-    uint64_t* k_empty = bar + 6;   // [2]
-    uint64_t* v_full = bar + 8;    // [2]
-    uint64_t* v_empty = bar + 10;  // [2]
-    uint64_t* s_full = bar + 12;   // [2]
-    uint64_t* s_free = bar + 14;   // [2]
-    // [2] P_g stored (indexed by g & 1): a softmax warp that skips the rescale wait can reach
-    // tile g + 1 (its S is issued before P V_g) and arrive while slower warps are still on tile g,
-    // so one barrier would complete the phase of tile g without them
-    uint64_t* p_full = bar + 16;
-    uint64_t* o_full = bar + 18;  // [2] O buffer of an item complete
-    uint64_t* o_free = bar + 20;  // [2] softmax warps have drained an O buffer
-    uint64_t* pv_done = bar + 22;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 23);
-    // O epilogue: per softmax warp a 32 x 32 bf16 slab (SWIZZLE_64B image) -> TMA bulk tensor store
-    uint8_t* slabs = sm + 6 * kTile + 1024;
-    constexpr int kSoft = 4 * kParts;  // softmax warps: 4 row quarters x kParts key slices
-    constexpr int kC = 128 / kParts;   // keys (and O columns) per softmax thread
-    // statically shared (not carved from the aligned dynamic block) so the compiler emits LDS/STS
-    __shared__ float xmax[2 * kParts * 128];  // [2 parity][kParts][128 rows]
-    __shared__ float xsum[kParts * 128];      // [kParts][128 rows]
+    uint8_t* sQ = sm;                          // one Q tile (32 KB)
+    uint8_t* sK = sm + kTile;                  // [2] x 16 KB
+    uint8_t* sV = sm + kTile + 2 * kTileKV;    // [2] x 16 KB
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + kTile + 4 * kTileKV);
+    uint64_t* q_full = bar;
+    uint64_t* q_empty = bar + 1;
+    uint64_t* k_full = bar + 2;    // [2]
+    uint64_t* k_empty = bar + 4;   // [2]
+    uint64_t* v_full = bar + 6;    // [2]
+    uint64_t* v_empty = bar + 8;   // [2]
+    uint64_t* s_full = bar + 10;   // [2]
+    uint64_t* s_free = bar + 12;   // [2]
+    uint64_t* p_full = bar + 14;   // [2] (by tile parity, see the kernel above)
+    uint64_t* o_full = bar + 16;
+    uint64_t* o_free = bar + 17;
+    uint64_t* pv_done = bar + 18;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bar + 19);
+    uint8_t* slabs = sm + kTile + 4 * kTileKV + 1024;  // 4 softmax warps x 2 KB (32 x 32 bf16, SWIZZLE_64B)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     FwdItems items{A.s / kT, A.nh, A.B, (A.s / kT) * A.nh * A.B, (int)gridDim.x, (int)blockIdx.x};
     const int n_items = items.count();
 
-    if (warp == 0 && lane == 0) {
-        for (const CUtensorMap* m : {&tmQ, &tmK, &tmV})
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&q_full[i]), 1);
-            mbar_init(smem_u32(&q_empty[i]), 1);
-            mbar_init(smem_u32(&k_full[i]), 1);
-            mbar_init(smem_u32(&k_empty[i]), 1);
-            mbar_init(smem_u32(&v_full[i]), 1);
-            mbar_init(smem_u32(&v_empty[i]), 1);
-            mbar_init(smem_u32(&s_full[i]), 1);
-            mbar_init(smem_u32(&s_free[i]), kSoft);
+    if (warp == 0) {
+        if (lane == 0) {
+            for (const CUtensorMap* m : {&tmQ, &tmK, &tmV})
+                asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
+            mbar_init(smem_u32(q_full), 1);
+            mbar_init(smem_u32(q_empty), 1);
+            for (int i = 0; i < 2; ++i) {
+                mbar_init(smem_u32(&k_full[i]), 1);
+                mbar_init(smem_u32(&k_empty[i]), 1);
+                mbar_init(smem_u32(&v_full[i]), 1);
+                mbar_init(smem_u32(&v_empty[i]), 1);
+                mbar_init(smem_u32(&s_full[i]), 1);
+                mbar_init(smem_u32(&s_free[i]), 4);
+                mbar_init(smem_u32(&p_full[i]), 4);
+            }
+            mbar_init(smem_u32(o_full), 1);
+            mbar_init(smem_u32(o_free), 4);
+            mbar_init(smem_u32(pv_done), 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        mbar_init(smem_u32(pv_done), 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(smem_u32(&p_full[i]), kSoft);
-            mbar_init(smem_u32(&o_full[i]), 1);
-            mbar_init(smem_u32(&o_free[i]), kSoft);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    if (warp == 2) {
+        __syncwarp();
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
-                     "r"(512));
+                     "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     fence_before();
     __syncthreads();
     fence_after();
-    const uint32_t tmem = *tmem_holder;  // S/P[0] 0-127, S/P[1] 128-255, O[0] 256-383, O[1] 384-511
-    pdl_launch_dependents();  // setup above overlapped the previous kernel (PDL); data from here on
+    const uint32_t tmem = *tmem_holder;  // S/P[0] 0-63, S/P[1] 64-127, O 128-255
+    pdl_launch_dependents();
     pdl_wait();
 
     if (warp == 0) {
-        if (lane == 0) {  // ===== TMA producer =====
+        if (lane == 0) {  // ===== TMA producer: Q per item, K / V per 64-key tile =====
             uint32_t g = 0;
             for (int it = 0; it < n_items; ++it) {
                 int qt, head, b;
                 items.get(it, qt, head, b);
-                const int qs = it & 1;
-                mbar_wait(smem_u32(&q_empty[qs]), ((it >> 1) & 1) ^ 1);
-                mbar_expect_tx(smem_u32(&q_full[qs]), kTile);
-                load_tile(smem_u32(sQ + qs * kTile), &tmQ, smem_u32(&q_full[qs]), qt * kT, head, b);
-                for (int j = 0; j <= qt; ++j, ++g) {
+                mbar_wait(smem_u32(q_empty), ((uint32_t)it & 1) ^ 1);
+                mbar_expect_tx(smem_u32(q_full), kTile);
+                load_tile(smem_u32(sQ), &tmQ, smem_u32(q_full), qt * kT, head, b);
+                const int nk = 2 * qt + 2;
+                for (int j = 0; j < nk; ++j, ++g) {
                     const int st = g & 1;
                     const uint32_t ph = (g >> 1) & 1;
                     mbar_wait(smem_u32(&k_empty[st]), ph ^ 1);
-                    mbar_expect_tx(smem_u32(&k_full[st]), kTile);
-                    load_tile(smem_u32(sK + st * kTile), &tmK, smem_u32(&k_full[st]), j * kT, head, b);
+                    mbar_expect_tx(smem_u32(&k_full[st]), kTileKV);
+                    load_kv(smem_u32(sK + st * kTileKV), &tmK, smem_u32(&k_full[st]), j * kKT, head, b);
                     mbar_wait(smem_u32(&v_empty[st]), ph ^ 1);
-                    mbar_expect_tx(smem_u32(&v_full[st]), kTile);
-                    load_tile(smem_u32(sV + st * kTile), &tmV, smem_u32(&v_full[st]), j * kT, head, b);
+                    mbar_expect_tx(smem_u32(&v_full[st]), kTileKV);
+                    load_kv(smem_u32(sV + st * kTileKV), &tmV, smem_u32(&v_full[st]), j * kKT, head, b);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // ===== MMA issuer: S(g+1) ahead of P(g) V(g), across items =====
-            constexpr uint32_t idS = idesc_bf16(128, 128, 0, 0);  // Q (K-major) x K^T (K-major)
+            constexpr uint32_t idS = idesc_bf16(128, kKT, 0, 0);  // Q (K-major) x K^T (K-major)
             constexpr uint32_t idO = idesc_bf16(128, 128, 0, 1);  // P (TMEM, K-major) x V (MN-major)
-            // cursor over this CTA's tiles: (item, j) and the global tile index g
-            int s_it = 0, s_j = 0, s_qt = 0;
+            int s_it = 0, s_j = 0, s_nk = 0;
             uint32_t s_g = 0;
-            auto issue_next_S = [&]() {  // S of the tile at the S cursor, then advance it
-                const int qs = s_it & 1, st = s_g & 1;
+            auto issue_next_S = [&]() {
+                const int st = s_g & 1;
                 const uint32_t ph = (s_g >> 1) & 1;
                 if (s_j == 0) {
-                    int h_, b_;
-                    items.get(s_it, s_qt, h_, b_);
-                    mbar_wait(smem_u32(&q_full[qs]), (s_it >> 1) & 1);
+                    int qt_, h_, b_;
+                    items.get(s_it, qt_, h_, b_);
+                    s_nk = 2 * qt_ + 2;
+                    mbar_wait(smem_u32(q_full), (uint32_t)s_it & 1);
                 }
                 mbar_wait(smem_u32(&k_full[st]), ph);
                 mbar_wait(smem_u32(&s_free[st]), ph ^ 1);
                 fence_after();
-                const uint32_t qa = smem_u32(sQ + qs * kTile), ka = smem_u32(sK + st * kTile);
+                const uint32_t qa = smem_u32(sQ), ka = smem_u32(sK + st * kTileKV);
 #pragma unroll
-                for (int t = 0; t < 8; ++t) mma_f16(tmem + st * 128, kdesc(qa, t), kdesc(ka, t), idS, t > 0);
+                for (int t = 0; t < 8; ++t) mma_f16(tmem + st * kKT, kdesc(qa, t), kdesc_kv(ka, t), idS, t > 0);
                 commit(smem_u32(&s_full[st]));
                 commit(smem_u32(&k_empty[st]));
-                if (s_j == s_qt) {  // last score tile of the item: its Q buffer is free after this MMA
-                    commit(smem_u32(&q_empty[qs]));
+                if (++s_j == s_nk) {  // the item's last score tile: its Q buffer is free after this MMA
+                    commit(smem_u32(q_empty));
                     s_j = 0;
                     ++s_it;
-                } else {
-                    ++s_j;
                 }
                 ++s_g;
             };
@@ -239,54 +354,43 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             for (int it = 0; it < n_items; ++it) {
                 int qt, head, b;
                 items.get(it, qt, head, b);
-                const uint32_t o_acc = tmem + 256 + (it & 1) * 128;  // O double-buffered across items
-                for (int j = 0; j <= qt; ++j, ++g) {
+                const int nk = 2 * qt + 2;
+                for (int j = 0; j < nk; ++j, ++g) {
                     if (s_it < n_items) issue_next_S();  // scores of the next tile overlap softmax of this one
                     const int st = g & 1;
-                    if (j == 0 && it >= 2) mbar_wait(smem_u32(&o_free[it & 1]), ((it >> 1) & 1) ^ 1);
+                    if (j == 0 && it >= 1) mbar_wait(smem_u32(o_free), ((uint32_t)it - 1) & 1);  // O drained
                     mbar_wait(smem_u32(&p_full[st]), (g >> 1) & 1);
                     mbar_wait(smem_u32(&v_full[st]), (g >> 1) & 1);
                     fence_after();
-                    const uint32_t va = smem_u32(sV + st * kTile);
+                    const uint32_t va = smem_u32(sV + st * kTileKV);
 #pragma unroll
-                    for (int t = 0; t < 8; ++t)
-                        mma_f16_ts(o_acc, tmem + st * 128 + t * 8, mndesc(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
+                    for (int t = 0; t < 4; ++t)
+                        mma_f16_ts(tmem + 128, tmem + st * kKT + t * 8, mndesc_kv(va, t), idO, (j > 0 || t > 0) ? 1u : 0u);
                     commit(smem_u32(pv_done));
                     commit(smem_u32(&v_empty[st]));
                 }
-                commit(smem_u32(&o_full[it & 1]));
+                commit(smem_u32(o_full));
             }
         }
-    } else if (warp >= 4) {  // ===== online softmax / epilogue =====
-        const int part = (warp - 4) >> 2, quarter = warp & 3;  // keys / O columns [kC * part, kC * part + kC)
+    } else {  // ===== softmax / epilogue (warps 2-5), thread = query row 32 * quarter + lane =====
+        const int quarter = warp & 3;
         const int r = quarter * 32 + lane;
         const uint32_t lane_base = uint32_t(quarter * 32) << 16;
-        const int quad_bar = 1 + quarter;  // named barrier of the kParts warps of this row quarter
+        const uint32_t obuf = tmem + lane_base + 128;
         const float sl2 = A.sl2;
+        uint8_t* slab = slabs + (warp - 2) * 2048;
         uint32_t g = 0;
-        // epilogue of an item, deferred until the next item's first P is handed to the MMA so
-        // its O buffer is complete by then and the stores overlap the next item's tensor work
         int pend_it = -1;
         float pend_inv = 0.f;
-        int pend_col = 0, pend_row0 = 0;  // O column of this slice, first token row of the warp's 32 rows
-        uint8_t* slab = slabs + (warp - 4) * 2048;
+        int pend_col = 0, pend_row0 = 0;
         auto epilogue = [&]() {
-            const int buf = pend_it & 1;
-            mbar_wait(smem_u32(&o_full[buf]), (pend_it >> 1) & 1);
+            mbar_wait(smem_u32(o_full), (uint32_t)pend_it & 1);
             fence_after();
 #pragma unroll 1
-            for (int c = 0; c < kC / 32; ++c) {
+            for (int c = 0; c < 4; ++c) {
                 float v[32];
-                ld32(tmem + lane_base + 256 + buf * 128 + part * kC + c * 32, v);
+                ld32(obuf + c * 32, v);
                 const float inv = pend_inv;
-                if constexpr (kParts != 2) {  // pk4 (A/B variant): no smem left for slabs
-                    uint4* op = reinterpret_cast<uint4*>(A.O + (size_t)(pend_row0 + lane) * A.h + pend_col + c * 32);
-#pragma unroll
-                    for (int k8 = 0; k8 < 4; ++k8)
-                        op[k8] = make_uint4(pack_bf16x2_rn(v[8 * k8] * inv, v[8 * k8 + 1] * inv), pack_bf16x2_rn(v[8 * k8 + 2] * inv, v[8 * k8 + 3] * inv),
-                                            pack_bf16x2_rn(v[8 * k8 + 4] * inv, v[8 * k8 + 5] * inv), pack_bf16x2_rn(v[8 * k8 + 6] * inv, v[8 * k8 + 7] * inv));
-                    continue;
-                }
                 if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slab free
                 __syncwarp();
 #pragma unroll
@@ -306,107 +410,51 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
             }
             fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(smem_u32(&o_free[buf]));
+            if (lane == 0) mbar_arrive(smem_u32(o_free));
             pend_it = -1;
         };
         for (int it = 0; it < n_items; ++it) {
             int qt, head, b;
             items.get(it, qt, head, b);
             const int q = qt * kT + r;
-            float m_used = -INFINITY, l = 0.f;
-            for (int j = 0; j <= qt; ++j, ++g) {
+            const int nk = 2 * qt + 2;
+            float mb = -INFINITY, l = 0.f;
+            for (int j = 0; j < nk; ++j, ++g) {
                 const int st = g & 1;
                 mbar_wait(smem_u32(&s_full[st]), (g >> 1) & 1);
                 fence_after();
-                float v[kC];
-                if constexpr (kC == 64)
-                    ld64(tmem + lane_base + st * 128 + part * kC, *reinterpret_cast<float(*)[64]>(v));
-                else
-                    ld32(tmem + lane_base + st * 128 + part * kC, *reinterpret_cast<float(*)[32]>(v));
-                if (j == qt) {  // diagonal tile: keys > q are masked
-                    const int lim = q - j * kT - part * kC;
-#pragma unroll
-                    for (int i = 0; i < kC; ++i) v[i] = i <= lim ? v[i] : -INFINITY;
-                }
-                float mx[8];  // 8 independent chains
-#pragma unroll
-                for (int i = 0; i < 8; ++i) mx[i] = v[i];
-#pragma unroll
-                for (int i = 8; i < kC; ++i) mx[i & 7] = fmaxf(mx[i & 7], v[i]);
-                const float cm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                       fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-                xmax[(st * kParts + part) * 128 + r] = cm;
-                fence_before();
-                // every slice has its scores in registers past this barrier: P may overwrite S
-                asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");
-                fence_after();
-                if (lane == 0) mbar_arrive(smem_u32(&s_free[st]));
-                float mt = xmax[(st * kParts) * 128 + r];  // finite: key 0 <= q
-#pragma unroll
-                for (int pp = 1; pp < kParts; ++pp) mt = fmaxf(mt, xmax[(st * kParts + pp) * 128 + r]);
-                float alpha = 1.f;
-                bool rescale = false;
-                if (m_used == -INFINITY) {
-                    m_used = mt;
-                } else if ((mt - m_used) * sl2 > kRescaleLog2) {
-                    alpha = ex2_approx((m_used - mt) * sl2);
-                    l *= alpha;
-                    m_used = mt;
-                    rescale = true;
-                }
-                const float mb = m_used * sl2;
-                float w[kC / 2];  // packed bf16 pairs, bit-cast to float for tcgen05.st
-                unsigned long long ad2[2] = {0ull, 0ull};  // (even, odd) column partial sums
-                const unsigned long long s2 = f2pack(sl2, sl2), nb2 = f2pack(-mb, -mb);
-#pragma unroll
-                for (int i = 0; i < kC / 2; ++i) {
-                    float x0, x1;
-                    f2unpack(ffma2(f2pack(v[2 * i], v[2 * i + 1]), s2, nb2), x0, x1);
-                    const float p0 = ex2_approx(x0), p1 = ex2_approx(x1);
-                    const unsigned long long p2 = f2pack(p0, p1);
-                    ad2[i & 1] = fadd2(ad2[i & 1], p2);
-                    w[i] = __uint_as_float(pack_bf16x2_rn(p0, p1));
-                }
-                {
-                    float a0, a1, a2, a3;
-                    f2unpack(ad2[0], a0, a1);
-                    f2unpack(ad2[1], a2, a3);
-                    l += (a0 + a1) + (a2 + a3);
-                }
-                if (__any_sync(0xffffffffu, rescale)) {  // O += P V of tile g-1 must have landed
-                    mbar_wait(smem_u32(pv_done), (g - 1) & 1);
-                    fence_after();
+                const uint32_t sbuf = tmem + lane_base + st * kKT;
+                unsigned long long ad2[2] = {0ull, 0ull};
 #pragma unroll 1
-                    for (int c = 0; c < kC / 32; ++c) {
-                        float o[32];
-                        const uint32_t ta = tmem + lane_base + 256 + (it & 1) * 128 + part * kC + c * 32;
-                        ld32(ta, o);
+                for (int c = 0; c < 2; ++c) {
+                    const int cd = 2 * (j - 2 * qt) + c;  // 32-key chunk within the diagonal 128-key block (< 0: below it)
+                    if (cd < quarter)
+                        row_chunk<false, true>(c, sbuf, obuf, lane, j, g, sl2, mb, l, ad2, smem_u32(pv_done));
+                    else if (cd == quarter)
+                        row_chunk<true, false>(c, sbuf, obuf, lane, j, g, sl2, mb, l, ad2, smem_u32(pv_done));
+                    else {  // keys after this row quarter: all masked
+                        float z[16];
 #pragma unroll
-                        for (int i = 0; i < 32; ++i) o[i] *= alpha;
-                        st32(ta, o);
+                        for (int i = 0; i < 16; ++i) z[i] = 0.f;
+                        st16(sbuf + c * 16, z);
                     }
                 }
-                // P_j -> first 64 columns of its S buffer (this slice's kC keys = kC / 2 columns)
-                if constexpr (kC == 64)
-                    st32(tmem + lane_base + st * 128 + part * (kC / 2), *reinterpret_cast<float(*)[32]>(w));
-                else
-                    st16(tmem + lane_base + st * 128 + part * (kC / 2), *reinterpret_cast<float(*)[16]>(w));
+                float a0, a1, a2, a3;
+                f2unpack(ad2[0], a0, a1);
+                f2unpack(ad2[1], a2, a3);
+                l += (a0 + a1) + (a2 + a3);
                 fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(smem_u32(&p_full[st]));
-                if (pend_it >= 0) epilogue();  // previous item: its last P V was issued before this P
+                if (lane == 0) {
+                    mbar_arrive(smem_u32(&s_free[st]));
+                    mbar_arrive(smem_u32(&p_full[st]));
+                }
+                if (j == 0 && pend_it >= 0) epilogue();  // previous item: its last P V was issued before this P
             }
-            xsum[part * 128 + r] = l;
-            asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");
-            float lt = xsum[r];
-#pragma unroll
-            for (int pp = 1; pp < kParts; ++pp) lt += xsum[pp * 128 + r];
-            asm volatile("bar.sync %0, %1;" ::"r"(quad_bar), "n"(kParts * 32) : "memory");  // xsum reused next item
-            const float inv = 1.f / lt;
-            if (part == 0) A.lse2[((size_t)b * A.nh + head) * A.s + q] = fmaf(m_used, sl2, __log2f(lt));
+            A.lse2[((size_t)b * A.nh + head) * A.s + q] = mb + __log2f(l);
             pend_it = it;
-            pend_inv = inv;
-            pend_col = head * kHD + part * kC;
+            pend_inv = 1.f / l;
+            pend_col = head * kHD;
             pend_row0 = b * A.s + qt * kT + quarter * 32;
         }
         if (pend_it >= 0) epilogue();
@@ -414,9 +462,9 @@ flash_fwd_pk_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_consta
     }
     fence_before();
     __syncthreads();
-    if (warp == 2) {
+    if (warp == 0) {
         fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
     }
 }
 
@@ -841,12 +889,12 @@ EncodeFn encode() {
 }
 
 // Head view {hd, s, nh, B} of a [B][s][ld] bf16 buffer (ld = 3h for qkv, h for dO), box 64 x 128.
-bool head_view(CUtensorMap* m, const uint16_t* base, int s, int nh, int B, long long ld) {
+bool head_view(CUtensorMap* m, const uint16_t* base, int s, int nh, int B, long long ld, int box_rows = 128) {
     EncodeFn fn = encode();
     if (!fn) return false;
     cuuint64_t dims[4] = {(cuuint64_t)kHD, (cuuint64_t)s, (cuuint64_t)nh, (cuuint64_t)B};
     cuuint64_t strides[3] = {(cuuint64_t)ld * 2, (cuuint64_t)kHD * 2, (cuuint64_t)s * ld * 2};
-    cuuint32_t box[4] = {64, 128, 1, 1};
+    cuuint32_t box[4] = {64, (cuuint32_t)box_rows, 1, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint16_t*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -899,9 +947,9 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
                       cudaStream_t st) {
     if (!flash_supported(hd, s)) return cudaErrorInvalidValue;
     const int h = nh * hd;
-    CUtensorMap mq, mk, mv;
-    if (!head_view(&mq, qkv, s, nh, B, 3ll * h) || !head_view(&mk, qkv + h, s, nh, B, 3ll * h) ||
-        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h))
+    CUtensorMap mq, mk, mv;  // K / V in 64-key boxes (64-key score tiles)
+    if (!head_view(&mq, qkv, s, nh, B, 3ll * h) || !head_view(&mk, qkv + h, s, nh, B, 3ll * h, kKT) ||
+        !head_view(&mv, qkv + 2 * h, s, nh, B, 3ll * h, kKT))
         return cudaErrorInvalidValue;
     FwdParams a;
     a.s = s;
@@ -912,15 +960,15 @@ cudaError_t flash_fwd(const uint16_t* qkv, uint16_t* O, float* lse2, int B, int 
     a.O = O;
     a.lse2 = lse2;
     const int items = (s / kT) * nh * B;
-    const int grid = items < kNumSMs ? items : kNumSMs;
+    const int grid = items < 2 * kNumSMs ? items : 2 * kNumSMs;  // two CTAs per SM
     CUtensorMap mo;  // O [B*s][h], box 32 x 32, SWIZZLE_64B (the epilogue slabs)
     if (!rows_view(&mo, O, h, (long long)B * s, 32, CU_TENSOR_MAP_SWIZZLE_64B)) return cudaErrorInvalidValue;
-    // tiles | barriers (1 KB) | epilogue slabs (2 KB per softmax warp)
-    const size_t smem = 1024 + 6 * (size_t)kTile + 1024 + 8 * 2048;
+    // Q | K, V rings | barriers (1 KB) | epilogue slabs (2 KB per softmax warp)
+    const size_t smem = 1024 + (size_t)kTile + 4 * (size_t)kTileKV + 1024 + 4 * 2048;
     static bool cfg = false;
-    cudaError_t e = set_smem(flash_fwd_pk_kernel<2>, smem, cfg);
+    cudaError_t e = set_smem(flash_fwd_k64_kernel, smem, cfg);
     if (e != cudaSuccess) return e;
-    launch_ex(flash_fwd_pk_kernel<2>, dim3(grid), dim3((4 + 8) * 32), smem, st, 1, mq, mk, mv, mo, a);
+    launch_ex(flash_fwd_k64_kernel, dim3(grid), dim3(192), smem, st, 1, mq, mk, mv, mo, a);
     return launched(1);
 }
 
